@@ -1,0 +1,248 @@
+/*
+ * conserve_b200.h -- C-ABI of the B200-native ConServe co-serving data plane.
+ *
+ * This is the drop-in boundary for the hot path of the reference CPU simulator
+ * (/root/reference/proj, arXiv 2410.01228). The reference has no plugin/FFI
+ * layer; its seams are C++ calls inside SimEngine. Each export below replaces
+ * one of those calls (file:line into /root/reference), with plain pointers and
+ * sizes only -- no C++ or torch types cross this boundary.
+ *
+ *   reference seam                                   replaced by
+ *   ------------------------------------------------ ----------------------------
+ *   KvCacheManager(ClusterConfig,bool)  kv_cache.cpp:38-46      cs_create / cs_destroy
+ *   KvCacheManager::* (allocate, commit, rollback, evict,       cs_kv_*
+ *     release, stage, flush, prefetch, transfer-done, audit,
+ *     page_table_json)  kv_cache.hpp:97-173
+ *   oracle_latency(plan)  sim_engine.cpp:256 / perf_model.cpp:56-96   cs_forward_launch
+ *   exec_->signal_preempt()  sim_engine.cpp:130                 cs_preempt_signal
+ *   exec_->safepoint_check(layer)  sim_engine.cpp:149 /         cs_iter_wait (preempted_at)
+ *     preemption.cpp:95-114
+ *   TransferChannel::enqueue  kv_cache.cpp:23-36                real D2H/H2D streams; cs_job_*
+ *
+ * Conventions:
+ *   - Every function returns int status: CS_OK (0) or a negative CS_ERR_*.
+ *     No exception crosses the boundary; cs_last_error() gives a thread-local
+ *     message. The error kinds mirror the reference's exception types
+ *     (std::logic_error, std::invalid_argument, std::runtime_error,
+ *     ConfigError) so an adapter can rethrow the same type.
+ *   - The caller owns every host buffer it passes; the engine owns device
+ *     memory, the pinned host KV pool, streams and events.
+ *   - Single-threaded caller. cs_preempt_signal may be called
+ *     from any thread.
+ *   - Times are integer microseconds (coserve::UsecT, time.hpp:13-41).
+ */
+#ifndef CONSERVE_B200_H_
+#define CONSERVE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- status -- */
+enum {
+  CS_OK = 0,
+  CS_ERR_LOGIC = -1,        /* std::logic_error (unknown id, audit failure, ...) */
+  CS_ERR_INVALID = -2,      /* std::invalid_argument */
+  CS_ERR_RUNTIME = -3,      /* std::runtime_error */
+  CS_ERR_CONFIG = -4,       /* coserve::ConfigError */
+  CS_ERR_CUDA = -5,         /* CUDA / cuBLAS / NCCL failure */
+  CS_ERR_POOL = -6,         /* physical pool exhausted although byte accounting fit */
+  CS_ERR_NOT_READY = -7     /* asynchronous object not complete yet (poll) */
+};
+const char* cs_last_error(void);
+const char* cs_version(void);
+
+/* ---------------------------------------------------------------- config -- */
+/* Engine flags. */
+enum {
+  CS_FLAG_NO_MODEL = 1 << 0,     /* KV pool + checkpoint path only (no weights) */
+  CS_FLAG_CKPT_STAGED = 1 << 1,  /* checkpoint via device staging + DMA instead of
+                                    the zero-copy gather kernel */
+  CS_FLAG_RESTORE_KERNEL = 1 << 2, /* restore via zero-copy load kernel instead
+                                      of per-page DMA */
+  CS_FLAG_SYNC_DEBUG = 1 << 3    /* synchronize after every launch (debug) */
+};
+
+typedef struct cs_config {
+  /* --- model shape (Llama-style decoder; SURVEY.md 8 model table) --- */
+  int32_t num_layers;        /* == ClusterConfig::num_layers (config.hpp:34) */
+  int32_t hidden;
+  int32_t n_heads;           /* query heads (global, before sharding) */
+  int32_t n_kv_heads;        /* KV heads (global) */
+  int32_t head_dim;
+  int32_t ffn;
+  int32_t vocab;
+  float rope_theta;
+  float rms_eps;
+  uint64_t weight_seed;      /* seeded random-init weights */
+  uint64_t token_seed;       /* teacher-forced ids: id(req,pos) = hash(seed,req,pos) % vocab */
+  /* --- cluster (mirrors coserve::ClusterConfig, config.hpp:33-59) --- */
+  int64_t kv_bytes_per_token;    /* must equal 2*L*H_kv*d*2 (whole model) */
+  int64_t gpu_kv_capacity;       /* bytes, byte-granular accounting as reference */
+  int64_t host_kv_capacity;
+  double d2h_bandwidth;          /* bytes/s; only for the modelled job timeline */
+  double h2d_bandwidth;
+  double gather_cost_us;
+  int32_t page_tokens;           /* fixed at 16 (config.cpp:60) */
+  int32_t safepoint_interval_layers;
+  int64_t max_batched_tokens;
+  int32_t incremental;           /* SchedulerPolicy::incremental() */
+  int32_t instrumented;          /* SchedulerPolicy::instrumented() */
+  /* --- B200 data-plane sizing --- */
+  int64_t extra_blocks;          /* physical-pool slack over ceil(cap/page_bytes); <0 = auto */
+  int64_t extra_host_slots;      /* host-pool slack; <0 = auto */
+  int32_t max_entries;           /* max entries per plan (0 = 1024) */
+  int32_t layer_lookahead;       /* layers enqueued ahead of the device (0 = 2) */
+  /* --- sharding (KV-head groups) --- */
+  int32_t tp_rank;
+  int32_t tp_size;
+  int32_t device;
+  int32_t flags;                 /* CS_FLAG_* */
+} cs_config;
+
+/* Fills *cfg with the reference defaults (config.hpp:33-59) and the tiny
+ * config-1 model shape; callers override fields. */
+void cs_config_default(cs_config* cfg);
+
+typedef struct cs_engine cs_engine;
+
+int cs_create(const cs_config* cfg, cs_engine** out);
+int cs_destroy(cs_engine* e);
+/* NCCL communicator for tp_size > 1: rank 0 calls cs_nccl_unique_id, the
+ * caller broadcasts the 128 bytes, every rank calls cs_nccl_init. */
+int cs_nccl_unique_id(uint8_t out_id[128]);
+int cs_nccl_init(cs_engine* e, const uint8_t id[128]);
+
+/* ------------------------------------------- KV block pool (C1 + C2 rows) -- */
+/* Mirrors coserve::AllocResult / EvictStats / ResumeCost / TransferJob /
+ * TransferDoneEffects (kv_cache.hpp:44-95). */
+typedef struct { int32_t ok; int64_t shortfall_pages; } cs_alloc_result;
+typedef struct { int64_t freed_pages, pending_pages, discarded_tokens; } cs_evict_stats;
+typedef struct { int64_t host_only_pages, host_only_bytes, discarded_tokens; } cs_resume_cost;
+enum { CS_D2H = 0, CS_H2D = 1 };
+typedef struct {
+  int64_t id;
+  int32_t direction;       /* CS_D2H / CS_H2D */
+  int64_t bytes;           /* reference byte count (known-token accounting) */
+  int64_t enqueue_time, start_time, done_time;   /* modelled FIFO timeline (us) */
+  double transfer_us, gather_us;
+  int64_t moved_bytes;     /* bytes this rank actually moved over the host link */
+} cs_transfer_job;
+typedef struct {
+  int64_t freed_pages;
+  int32_t n_became_resident;
+  int64_t became_resident[4];
+} cs_transfer_done;
+
+int cs_kv_register_request(cs_engine* e, int64_t id, int32_t online);
+int cs_kv_allocate(cs_engine* e, int64_t id, int64_t n_tokens, int64_t now, cs_alloc_result* out);
+int cs_kv_commit(cs_engine* e, int64_t id);
+int cs_kv_rollback(cs_engine* e, int64_t id);
+int cs_kv_evict_request_gpu(cs_engine* e, int64_t id, int64_t now, int64_t max_pages, cs_evict_stats* out);
+int cs_kv_discard_request(cs_engine* e, int64_t id, int64_t now, cs_evict_stats* out);
+/* ReleaseStats: freed pages plus (owner, discarded tokens) pairs written to
+ * discards[2*i], discards[2*i+1] (capacity cap pairs; *n_discards = count). */
+int cs_kv_release_offline_pages_on_demand(cs_engine* e, int64_t needed_pages, int64_t now,
+                                          int64_t* freed_pages, int64_t* discards,
+                                          int64_t cap, int64_t* n_discards);
+int cs_kv_releasable_offline_pages_now(cs_engine* e, int64_t* out);
+int cs_kv_stage_checkpoint(cs_engine* e, int64_t id, int64_t from_token, int64_t to_token);
+/* Coalesces staged deltas into one D2H job (kv_cache.cpp:364-400) and launches
+ * the gather on the D2H stream behind the last forward. *has_job = 0 if none. */
+int cs_kv_flush_checkpoints(cs_engine* e, int64_t now, cs_transfer_job* job, int32_t* has_job);
+int cs_kv_resume_cost(cs_engine* e, int64_t id, cs_resume_cost* out);
+int cs_kv_fully_resident(cs_engine* e, int64_t id, int32_t* out);
+int cs_kv_prefetch_inflight(cs_engine* e, int64_t id, int32_t* out);
+/* Restore all HostOnly pages of one request into newly allocated blocks
+ * (kv_cache.cpp:428-455), H2D on its own stream. */
+int cs_kv_start_prefetch(cs_engine* e, int64_t id, int64_t now, cs_transfer_job* job, int32_t* has_job);
+int cs_kv_recompute_chunk(cs_engine* e, int64_t id, int64_t desired, int64_t cap, int64_t* out);
+/* Completion (kv_cache.cpp:471-520). Blocks until the real transfer's event
+ * has completed, then applies the bookkeeping. */
+int cs_kv_on_transfer_done(cs_engine* e, int64_t job_id, int64_t now, cs_transfer_done* out);
+int cs_kv_on_request_paused(cs_engine* e, int64_t id, uint64_t pause_seq);
+int cs_kv_on_request_active(cs_engine* e, int64_t id);
+int cs_kv_release_request(cs_engine* e, int64_t id);
+/* Declares that the last forward wrote KV positions [w0, w1) of request id;
+ * cs_iter_wait calls this itself for surviving entries. Used to map the
+ * reference's known-token checkpoint ranges onto written positions
+ * (SURVEY.md 0 item 11). */
+int cs_kv_note_written(cs_engine* e, int64_t id, int64_t w0, int64_t w1);
+
+typedef struct {
+  int64_t gpu_used_bytes, gpu_free_bytes, host_used_bytes, gpu_free_pages, page_bytes;
+  int64_t total_d2h_bytes, total_h2d_bytes, recompute_tagged_tokens;
+  int32_t transfers_inflight;
+  /* physical state (B200 only) */
+  int64_t n_blocks, free_blocks, quarantined_blocks, n_host_slots, free_host_slots;
+  int64_t moved_d2h_bytes, moved_h2d_bytes;
+  int64_t nonresident_reads;     /* block-table reads of pages the reference marks non-resident (D3) */
+} cs_kv_stats;
+int cs_kv_stats_get(cs_engine* e, cs_kv_stats* out);
+int cs_kv_request_info(cs_engine* e, int64_t id, int64_t* gpu_pages, int64_t* covered_tokens,
+                       int64_t* pending_append_tokens);
+/* Deep invariant check (kv_cache.cpp:566-620) plus the physical invariants
+ * (every resident page owns a distinct block, free-list partition). */
+int cs_kv_audit(cs_engine* e);
+/* Same JSON as KvCacheManager::page_table_json (kv_cache.cpp:622-634). */
+int cs_kv_page_table_json(cs_engine* e, int64_t id, char* buf, size_t cap, size_t* len);
+/* Physical block ids (-1 = not resident) and host slot ids (-1 = none), one
+ * per logical page. */
+int cs_kv_block_table(cs_engine* e, int64_t id, int32_t* blocks, int32_t* slots, int64_t cap, int64_t* n);
+
+/* -------------------------------- forward over a mixed batch (A1/A2/A5) -- */
+/* Mirrors coserve::BatchEntry (perf_model.hpp:15-21); EntryKind order kept. */
+enum { CS_PREFILL = 0, CS_DECODE = 1, CS_RECOMPUTE = 2 };
+typedef struct {
+  int64_t request_id;
+  int64_t compute_tokens;   /* P */
+  int64_t context_tokens;   /* C */
+  int32_t kind;
+  int32_t online;
+} cs_batch_entry;
+
+typedef struct {
+  int32_t n_outputs;          /* sampled rows (decode + final prefill chunks) */
+  int32_t preempted_at_layer; /* -1 if not preempted */
+  int32_t n_entries_after;    /* entries that ran to the end */
+  int32_t done;
+  double gpu_ms;              /* device time of the iteration (events) */
+  double preempt_signal_to_drop_us; /* host flag store -> device observed (mapped clock) */
+} cs_iter_info;
+
+/* Launches the L-layer forward for one plan (online entries must form a
+ * prefix, scheduler.cpp:183-317). Asynchronous. epoch tags the iteration
+ * for the preemption flag. Outputs (argmax ids, one per
+ * sampled row, entry order) are copied to out_tokens at cs_iter_wait. */
+int cs_forward_launch(cs_engine* e, const cs_batch_entry* entries, int32_t n, uint64_t epoch);
+/* Host flag store: drop offline entries at the next safepoint of the
+ * iteration tagged epoch (preemption.cpp:95-114). */
+int cs_preempt_signal(cs_engine* e, uint64_t epoch);
+/* Waits for the running iteration. out_tokens (cap entries) receives sampled
+ * ids; logits (optional, n_outputs x vocab fp32) the raw logits. Marks KV
+ * written for surviving entries and releases quarantined blocks. */
+int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t cap, float* logits);
+int cs_iter_poll(cs_engine* e, int32_t* done);
+
+/* ------------------------------------------------------- test / bench hooks -- */
+/* Copies one physical block (all layers of this rank's shard) to host. */
+int cs_debug_read_block(cs_engine* e, int32_t block, void* dst, size_t bytes);
+int cs_debug_write_block(cs_engine* e, int32_t block, const void* src, size_t bytes);
+/* Host pool slot contents (this rank's shard of one page). */
+int cs_debug_read_host_slot(cs_engine* e, int32_t slot, void* dst, size_t bytes);
+/* Fill every block with a deterministic pattern (seeded). */
+int cs_debug_fill_pool(cs_engine* e, uint64_t seed);
+/* Last-layer hidden/attention outputs of the last iteration for parity. */
+int cs_debug_read_attn_out(cs_engine* e, int32_t layer, void* dst, size_t bytes);
+int cs_debug_set_capture_layer(cs_engine* e, int32_t layer);
+/* Model weights (bf16 bits) for parity: tensor index per cs_weight enum. */
+int cs_debug_read_weight(cs_engine* e, int32_t layer, int32_t which, void* dst, size_t bytes, size_t* needed);
+int cs_sync(cs_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CONSERVE_B200_H_ */
