@@ -59,11 +59,13 @@ const char* cs_version(void);
 /* Engine flags. */
 enum {
   CS_FLAG_NO_MODEL = 1 << 0,     /* KV pool + checkpoint path only (no weights) */
-  CS_FLAG_CKPT_STAGED = 1 << 1,  /* checkpoint via device staging + DMA instead of
-                                    the zero-copy gather kernel */
-  CS_FLAG_RESTORE_KERNEL = 1 << 2, /* restore via zero-copy load kernel instead
-                                      of per-page DMA */
-  CS_FLAG_SYNC_DEBUG = 1 << 3    /* synchronize after every launch (debug) */
+  CS_FLAG_RESERVED1 = 1 << 1,
+  CS_FLAG_RESERVED2 = 1 << 2,
+  CS_FLAG_SYNC_DEBUG = 1 << 3,   /* synchronize after every launch (debug) */
+  CS_FLAG_HOST_ONLY = 1 << 4,    /* bookkeeping only: no CUDA calls at all
+                                    (CPU tests, oracle-clock shadow runs) */
+  CS_FLAG_NO_FWD_QUARANTINE = 1 << 5 /* freed blocks need no forward to drain
+                                        (bookkeeping-only call sequences) */
 };
 
 typedef struct cs_config {
@@ -180,6 +182,7 @@ typedef struct {
   int64_t n_blocks, free_blocks, quarantined_blocks, n_host_slots, free_host_slots;
   int64_t moved_d2h_bytes, moved_h2d_bytes;
   int64_t nonresident_reads;     /* block-table reads of pages the reference marks non-resident (D3) */
+  double moved_d2h_ms, moved_h2d_ms;  /* summed device time of the gather / scatter kernels */
 } cs_kv_stats;
 int cs_kv_stats_get(cs_engine* e, cs_kv_stats* out);
 int cs_kv_request_info(cs_engine* e, int64_t id, int64_t* gpu_pages, int64_t* covered_tokens,
@@ -235,12 +238,18 @@ int cs_debug_write_block(cs_engine* e, int32_t block, const void* src, size_t by
 int cs_debug_read_host_slot(cs_engine* e, int32_t slot, void* dst, size_t bytes);
 /* Fill every block with a deterministic pattern (seeded). */
 int cs_debug_fill_pool(cs_engine* e, uint64_t seed);
-/* Last-layer hidden/attention outputs of the last iteration for parity. */
-int cs_debug_read_attn_out(cs_engine* e, int32_t layer, void* dst, size_t bytes);
-int cs_debug_set_capture_layer(cs_engine* e, int32_t layer);
-/* Model weights (bf16 bits) for parity: tensor index per cs_weight enum. */
+/* which: 0 = attention output [T, Hq*d], 1 = residual stream x [T, hidden],
+ * 2 = qkv [T, (Hq+2Hkv)*d] (bf16, rank-local, last layer run). */
+int cs_debug_read_activation(cs_engine* e, int32_t which, void* dst, size_t bytes);
+/* Model weights (bf16 bits) for parity. which: 0 attn_norm, 1 wqkv, 2 wo,
+ * 3 mlp_norm, 4 w_gate_up, 5 w_down (per layer); 6 embedding, 7 lm_head,
+ * 8 final_norm. *needed receives the byte size. */
 int cs_debug_read_weight(cs_engine* e, int32_t layer, int32_t which, void* dst, size_t bytes, size_t* needed);
 int cs_sync(cs_engine* e);
+/* Host copies of the device hashes (teacher-forced ids, weight init) so a CPU
+ * oracle can be checked against them without a GPU. */
+int32_t cs_token_id(uint64_t seed, int64_t req, int64_t pos, int32_t vocab);
+float cs_hash_uniform(uint64_t seed, uint64_t tensor, uint64_t idx);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,474 @@
+// Paged attention over the block-table-indexed KV pool.
+//
+// K1 attn_decode: single-query rows (decode entries and 1-token chunks) --
+//   query position p attends keys [0, p]. One CTA per (entry, KV head,
+//   split); the G query heads of the KV group are the MMA's M rows, so every
+//   K/V byte is read from HBM once per group. Each warp streams whole 16-token
+//   pages through a private 2-stage cp.async ring (16-byte coalesced loads,
+//   XOR-swizzled smem) and keeps its own online softmax; warps and splits are
+//   merged at the end. HBM-bound: the contractions run on mma.sync only to
+//   keep the instruction count far below the byte rate.
+// K2 attn_prefill: multi-query chunks (prefill / recompute) -- FlashAttention-2
+//   style tiles of 64 packed (token, head-in-group) rows x 64 keys with a
+//   causal mask on absolute positions (recompute positions may be
+//   non-contiguous). First version on mma.sync; tcgen05 version: attn_tc.cu.
+#include "common.cuh"
+
+namespace csk {
+
+namespace {
+
+constexpr int kPage = 16;
+
+__device__ __forceinline__ const __nv_bfloat16* kv_page(const AttnParams& p, int32_t block, int kvh, int which,
+                                                         int D) {
+  const size_t layer_elems = static_cast<size_t>(2) * p.hkv * kPage * D;
+  return p.pool + (static_cast<size_t>(block) * p.num_layers + p.layer) * layer_elems +
+         (static_cast<size_t>(which) * p.hkv + kvh) * kPage * D;
+}
+
+template <int D>
+__device__ __forceinline__ void load_page_async(uint8_t* sK, uint8_t* sV, const __nv_bfloat16* k,
+                                                const __nv_bfloat16* v, int lane) {
+  constexpr int CH = D / 8;  // 16-byte chunks per row
+#pragma unroll
+  for (int i = 0; i < (kPage * CH) / 32; ++i) {
+    const int c = lane + 32 * i;
+    const int r = c / CH, ch = c % CH;
+    cp_async16(sK + swz<D>(r, ch), k + r * D + ch * 8);
+    cp_async16(sV + swz<D>(r, ch), v + r * D + ch * 8);
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------- K1 ----
+template <int D, int G>
+__global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
+  constexpr int KS = D / 16;
+  constexpr int NTD = D / 8;
+  constexpr int PB = kPage * D * 2;  // bytes per K (or V) page
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int split = blockIdx.x, kvh = blockIdx.y, di = blockIdx.z;
+  if (di >= p.desc->n_dec_cur) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int ent = p.dec_ent[di];
+  const int row = p.ent_q0[ent];
+  const int kv_len = p.ent_kvlen[ent];
+  const int n_pages = (kv_len + kPage - 1) / kPage;
+  const int pg0 = split * p.pages_per_split;
+  const int pg1 = min(n_pages, pg0 + p.pages_per_split);
+  const int32_t* bt = p.block_table + p.ent_bt[ent];
+
+  uint32_t qa[KS][4];
+  {
+    const __nv_bfloat16* q = p.qkv + static_cast<size_t>(row) * p.qkv_stride + static_cast<size_t>(kvh) * G * D;
+    const int r0 = gid, r1 = gid + 8;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int d0 = ks * 16 + tig * 2;
+      qa[ks][0] = r0 < G ? *reinterpret_cast<const uint32_t*>(q + r0 * D + d0) : 0u;
+      qa[ks][1] = r1 < G ? *reinterpret_cast<const uint32_t*>(q + r1 * D + d0) : 0u;
+      qa[ks][2] = r0 < G ? *reinterpret_cast<const uint32_t*>(q + r0 * D + d0 + 8) : 0u;
+      qa[ks][3] = r1 < G ? *reinterpret_cast<const uint32_t*>(q + r1 * D + d0 + 8) : 0u;
+    }
+  }
+
+  float o[NTD][4];
+#pragma unroll
+  for (int i = 0; i < NTD; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  uint8_t* wbuf = smem + warp * 4 * PB;  // [stage][K|V]
+  int pg = pg0 + warp;
+  if (pg < pg1) {
+    load_page_async<D>(wbuf, wbuf + PB, kv_page(p, bt[pg], kvh, 0, D), kv_page(p, bt[pg], kvh, 1, D), lane);
+  }
+  cp_async_commit();
+  int stage = 0;
+  for (; pg < pg1; pg += 4) {
+    const int nxt = pg + 4;
+    if (nxt < pg1) {
+      uint8_t* nb = wbuf + (stage ^ 1) * 2 * PB;
+      load_page_async<D>(nb, nb + PB, kv_page(p, bt[nxt], kvh, 0, D), kv_page(p, bt[nxt], kvh, 1, D), lane);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const uint8_t* sK = wbuf + stage * 2 * PB;
+    const uint8_t* sV = sK + PB;
+
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int mi = lane >> 3;
+      const int tok = (mi >> 1) * 8 + (lane & 7);
+      uint32_t b0, b1, b2, b3;
+      ldmatrix_x4(b0, b1, b2, b3, sK + swz<D>(tok, ks * 2 + (mi & 1)));
+      mma_bf16_16816(s[0], qa[ks], b0, b1);
+      mma_bf16_16816(s[1], qa[ks], b2, b3);
+    }
+    const int base = pg * kPage;
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const bool ok = base + nt * 8 + tig * 2 + j < kv_len;
+        s[nt][j] = ok ? s[nt][j] * p.scale_log2 : -INFINITY;
+        s[nt][2 + j] = ok ? s[nt][2 + j] * p.scale_log2 : -INFINITY;
+        mx0 = fmaxf(mx0, s[nt][j]);
+        mx1 = fmaxf(mx1, s[nt][2 + j]);
+      }
+    }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
+    m0 = mn0;
+    m1 = mn1;
+    uint32_t pa[4];
+    float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const float p0 = exp2f(s[nt][0] - mn0), p1 = exp2f(s[nt][1] - mn0);
+      const float p2 = exp2f(s[nt][2] - mn1), p3 = exp2f(s[nt][3] - mn1);
+      rs0 += p0 + p1;
+      rs1 += p2 + p3;
+      pa[nt * 2 + 0] = pack_bf16(p0, p1);
+      pa[nt * 2 + 1] = pack_bf16(p2, p3);
+    }
+    l0 = l0 * al0 + rs0;
+    l1 = l1 * al1 + rs1;
+#pragma unroll
+    for (int i = 0; i < NTD; ++i) {
+      o[i][0] *= al0;
+      o[i][1] *= al0;
+      o[i][2] *= al1;
+      o[i][3] *= al1;
+    }
+#pragma unroll
+    for (int nd = 0; nd < D / 16; ++nd) {
+      const int mi = lane >> 3;
+      const int tok = (mi & 1) * 8 + (lane & 7);
+      uint32_t v0, v1, v2, v3;
+      ldmatrix_x4_trans(v0, v1, v2, v3, sV + swz<D>(tok, nd * 2 + (mi >> 1)));
+      mma_bf16_16816(o[nd * 2], pa, v0, v1);
+      mma_bf16_16816(o[nd * 2 + 1], pa, v2, v3);
+    }
+    __syncwarp();
+    stage ^= 1;
+  }
+  cp_async_wait<0>();
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+
+  // Merge the 4 warps: [warp][16 rows] m, l and [warp][16][D] partial O.
+  __syncthreads();
+  float* sm_m = reinterpret_cast<float*>(smem);
+  float* sm_l = sm_m + 4 * 16;
+  float* sm_o = sm_l + 4 * 16;
+  if (tig == 0) {
+    sm_m[warp * 16 + gid] = m0;
+    sm_m[warp * 16 + gid + 8] = m1;
+    sm_l[warp * 16 + gid] = l0;
+    sm_l[warp * 16 + gid + 8] = l1;
+  }
+#pragma unroll
+  for (int nt = 0; nt < NTD; ++nt) {
+    const int d = nt * 8 + tig * 2;
+    sm_o[(warp * 16 + gid) * D + d] = o[nt][0];
+    sm_o[(warp * 16 + gid) * D + d + 1] = o[nt][1];
+    sm_o[(warp * 16 + gid + 8) * D + d] = o[nt][2];
+    sm_o[(warp * 16 + gid + 8) * D + d + 1] = o[nt][3];
+  }
+  __syncthreads();
+  const int S = p.n_splits;
+  const size_t item = (static_cast<size_t>(di) * p.hkv + kvh) * S + split;
+  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+    const int r = idx / D, d = idx % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w * 16 + r]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float f = exp2f(sm_m[w * 16 + r] - M);
+        L += sm_l[w * 16 + r] * f;
+        O += sm_o[(w * 16 + r) * D + d] * f;
+      }
+    }
+    if (S == 1) {
+      p.out[static_cast<size_t>(row) * p.hq * D + static_cast<size_t>(kvh * G + r) * D + d] =
+          __float2bfloat16(L > 0.f ? O / L : 0.f);
+    } else {
+      float* wm = p.ws + item * G * 2;
+      float* wo = p.ws + static_cast<size_t>(gridDim.z) * p.hkv * S * G * 2 + item * G * D;
+      if (d == 0) {
+        wm[r * 2] = M;
+        wm[r * 2 + 1] = L;
+      }
+      wo[r * D + d] = O;
+    }
+  }
+}
+
+// Split-K merge for K1: one CTA per (entry, KV head), thread per (row, dim).
+template <int D, int G>
+__global__ void attn_decode_combine_kernel(AttnParams p, int n_dec_grid) {
+  const int kvh = blockIdx.y, di = blockIdx.x;
+  if (di >= p.desc->n_dec_cur) return;
+  const int S = p.n_splits;
+  const int ent = p.dec_ent[di];
+  const int row = p.ent_q0[ent];
+  const size_t base_item = (static_cast<size_t>(di) * p.hkv + kvh) * S;
+  const float* wm = p.ws + base_item * G * 2;
+  const float* wo = p.ws + static_cast<size_t>(n_dec_grid) * p.hkv * S * G * 2 + base_item * G * D;
+  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+    const int r = idx / D, d = idx % D;
+    float M = -INFINITY;
+    for (int s = 0; s < S; ++s) M = fmaxf(M, wm[(s * G + r) * 2]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+      for (int s = 0; s < S; ++s) {
+        const float ms = wm[(s * G + r) * 2];
+        if (ms == -INFINITY) continue;
+        const float f = exp2f(ms - M);
+        L += wm[(s * G + r) * 2 + 1] * f;
+        O += wo[(s * G + r) * D + d] * f;
+      }
+    }
+    p.out[static_cast<size_t>(row) * p.hq * D + static_cast<size_t>(kvh * G + r) * D + d] =
+        __float2bfloat16(L > 0.f ? O / L : 0.f);
+  }
+}
+
+// ------------------------------------------------------------------- K2 ----
+constexpr int kTileRows = 64;
+constexpr int kTileKeys = 64;
+
+template <int D, int G>
+__global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
+  constexpr int KS = D / 16;
+  constexpr int NTD = D / 8;
+  constexpr int TB = kTileKeys * D * 2;  // bytes per K (or V) tile
+  constexpr int CH = D / 8;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tile = blockIdx.x, kvh = blockIdx.y;
+  if (tile >= p.desc->n_pt_cur) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const PrefillTile t = p.tiles[tile];
+  const int ent = t.entry;
+  const int q0 = p.ent_q0[ent];
+  const int n_rows = p.ent_qlen[ent] * G;
+  const int kv_len = p.ent_kvlen[ent];
+  const int32_t* bt = p.block_table + p.ent_bt[ent];
+  const int n_pages = (kv_len + kPage - 1) / kPage;
+
+  // This thread's two rows.
+  const int ra = t.row0 + warp * 16 + gid, rb = ra + 8;
+  const bool va = ra < n_rows, vb = rb < n_rows;
+  const int last_row = min(t.row0 + kTileRows, n_rows) - 1;
+  const int kv_hi = min(kv_len, p.tok_pos[q0 + last_row / G] + 1);
+  const int pos_a = va ? p.tok_pos[q0 + ra / G] : kv_hi;
+  const int pos_b = vb ? p.tok_pos[q0 + rb / G] : kv_hi;
+
+  uint32_t qa[KS][4];
+  {
+    const __nv_bfloat16* qA = p.qkv + static_cast<size_t>(q0 + (va ? ra : 0) / G) * p.qkv_stride +
+                              static_cast<size_t>(kvh * G + (va ? ra : 0) % G) * D;
+    const __nv_bfloat16* qB = p.qkv + static_cast<size_t>(q0 + (vb ? rb : 0) / G) * p.qkv_stride +
+                              static_cast<size_t>(kvh * G + (vb ? rb : 0) % G) * D;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int d0 = ks * 16 + tig * 2;
+      qa[ks][0] = va ? *reinterpret_cast<const uint32_t*>(qA + d0) : 0u;
+      qa[ks][1] = vb ? *reinterpret_cast<const uint32_t*>(qB + d0) : 0u;
+      qa[ks][2] = va ? *reinterpret_cast<const uint32_t*>(qA + d0 + 8) : 0u;
+      qa[ks][3] = vb ? *reinterpret_cast<const uint32_t*>(qB + d0 + 8) : 0u;
+    }
+  }
+
+  auto load_tile = [&](int kt, int st) {
+    uint8_t* sK = smem + st * 2 * TB;
+    uint8_t* sV = sK + TB;
+#pragma unroll
+    for (int i = 0; i < (kTileKeys * CH) / 128; ++i) {
+      const int c = threadIdx.x + 128 * i;
+      const int r = c / CH, ch = c % CH;
+      const int pgi = kt * (kTileKeys / kPage) + r / kPage;
+      if (pgi < n_pages) {
+        const int32_t blk = bt[pgi];
+        cp_async16(sK + swz<D>(r, ch), kv_page(p, blk, kvh, 0, D) + (r % kPage) * D + ch * 8);
+        cp_async16(sV + swz<D>(r, ch), kv_page(p, blk, kvh, 1, D) + (r % kPage) * D + ch * 8);
+      } else {
+        *reinterpret_cast<uint4*>(sK + swz<D>(r, ch)) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(sV + swz<D>(r, ch)) = make_uint4(0, 0, 0, 0);
+      }
+    }
+  };
+
+  float o[NTD][4];
+#pragma unroll
+  for (int i = 0; i < NTD; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const int n_kt = (kv_hi + kTileKeys - 1) / kTileKeys;
+  load_tile(0, 0);
+  cp_async_commit();
+  for (int kt = 0; kt < n_kt; ++kt) {
+    const int st = kt & 1;
+    if (kt + 1 < n_kt) load_tile(kt + 1, st ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const uint8_t* sK = smem + st * 2 * TB;
+    const uint8_t* sV = sK + TB;
+    float s[kTileKeys / 8][4];
+#pragma unroll
+    for (int i = 0; i < kTileKeys / 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+      for (int np = 0; np < kTileKeys / 16; ++np) {
+        const int mi = lane >> 3;
+        const int key = np * 16 + (mi >> 1) * 8 + (lane & 7);
+        uint32_t b0, b1, b2, b3;
+        ldmatrix_x4(b0, b1, b2, b3, sK + swz<D>(key, ks * 2 + (mi & 1)));
+        mma_bf16_16816(s[np * 2], qa[ks], b0, b1);
+        mma_bf16_16816(s[np * 2 + 1], qa[ks], b2, b3);
+      }
+    }
+    const int kbase = kt * kTileKeys;
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < kTileKeys / 8; ++nt) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int key = kbase + nt * 8 + tig * 2 + j;
+        s[nt][j] = (key <= pos_a && key < kv_len) ? s[nt][j] * p.scale_log2 : -INFINITY;
+        s[nt][2 + j] = (key <= pos_b && key < kv_len) ? s[nt][2 + j] * p.scale_log2 : -INFINITY;
+        mx0 = fmaxf(mx0, s[nt][j]);
+        mx1 = fmaxf(mx1, s[nt][2 + j]);
+      }
+    }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float al0 = mn0 == -INFINITY ? 1.f : exp2f(m0 - mn0);
+    const float al1 = mn1 == -INFINITY ? 1.f : exp2f(m1 - mn1);
+    const float sub0 = mn0 == -INFINITY ? 0.f : mn0;
+    const float sub1 = mn1 == -INFINITY ? 0.f : mn1;
+    m0 = mn0;
+    m1 = mn1;
+    float rs0 = 0.f, rs1 = 0.f;
+    uint32_t pa[kTileKeys / 16][4];
+#pragma unroll
+    for (int nt = 0; nt < kTileKeys / 8; ++nt) {
+      const float p0 = exp2f(s[nt][0] - sub0), p1 = exp2f(s[nt][1] - sub0);
+      const float p2 = exp2f(s[nt][2] - sub1), p3 = exp2f(s[nt][3] - sub1);
+      rs0 += p0 + p1;
+      rs1 += p2 + p3;
+      pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
+      pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
+    }
+    l0 = l0 * al0 + rs0;
+    l1 = l1 * al1 + rs1;
+#pragma unroll
+    for (int i = 0; i < NTD; ++i) {
+      o[i][0] *= al0;
+      o[i][1] *= al0;
+      o[i][2] *= al1;
+      o[i][3] *= al1;
+    }
+#pragma unroll
+    for (int kk = 0; kk < kTileKeys / 16; ++kk) {
+#pragma unroll
+      for (int nd = 0; nd < D / 16; ++nd) {
+        const int mi = lane >> 3;
+        const int key = kk * 16 + (mi & 1) * 8 + (lane & 7);
+        uint32_t v0, v1, v2, v3;
+        ldmatrix_x4_trans(v0, v1, v2, v3, sV + swz<D>(key, nd * 2 + (mi >> 1)));
+        mma_bf16_16816(o[nd * 2], pa[kk], v0, v1);
+        mma_bf16_16816(o[nd * 2 + 1], pa[kk], v2, v3);
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
+  const size_t ostride = static_cast<size_t>(p.hq) * D;
+#pragma unroll
+  for (int nt = 0; nt < NTD; ++nt) {
+    const int d = nt * 8 + tig * 2;
+    if (va) {
+      __nv_bfloat16* dst = p.out + static_cast<size_t>(q0 + ra / G) * ostride + static_cast<size_t>(kvh * G + ra % G) * D + d;
+      *reinterpret_cast<uint32_t*>(dst) = pack_bf16(o[nt][0] * i0, o[nt][1] * i0);
+    }
+    if (vb) {
+      __nv_bfloat16* dst = p.out + static_cast<size_t>(q0 + rb / G) * ostride + static_cast<size_t>(kvh * G + rb % G) * D + d;
+      *reinterpret_cast<uint32_t*>(dst) = pack_bf16(o[nt][2] * i1, o[nt][3] * i1);
+    }
+  }
+}
+
+// ------------------------------------------------------------- launchers ----
+int decode_smem_bytes(int D) { return 4 * 4 * kPage * D * 2 > (4 * 16 * 2 + 4 * 16 * D) * 4 ? 4 * 4 * kPage * D * 2 : (4 * 16 * 2 + 4 * 16 * D) * 4; }
+int prefill_smem_bytes(int D) { return 2 * 2 * kTileKeys * D * 2; }
+
+template <int D, int G>
+static void launch_attention_t(const AttnParams& p, int n_dec_grid, int n_pt_grid, cudaStream_t s) {
+  if (n_dec_grid > 0) {
+    const int smem = decode_smem_bytes(D);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(attn_decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    dim3 grid(p.n_splits, p.hkv, n_dec_grid);
+    attn_decode_kernel<D, G><<<grid, 128, smem, s>>>(p);
+    if (p.n_splits > 1) attn_decode_combine_kernel<D, G><<<dim3(n_dec_grid, p.hkv), 128, 0, s>>>(p, n_dec_grid);
+  }
+  if (n_pt_grid > 0) {
+    const int smem = prefill_smem_bytes(D);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(attn_prefill_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    attn_prefill_kernel<D, G><<<dim3(n_pt_grid, p.hkv), 128, smem, s>>>(p);
+  }
+}
+
+// Dispatch on (head_dim, group size); returns false for an unsupported shape.
+bool launch_attention(const AttnParams& p, int head_dim, int group, int n_dec_grid, int n_pt_grid, cudaStream_t s) {
+#define CS_ATTN_CASE(DD, GG)                                    \
+  if (head_dim == DD && group == GG) {                          \
+    launch_attention_t<DD, GG>(p, n_dec_grid, n_pt_grid, s);    \
+    return true;                                                \
+  }
+  CS_ATTN_CASE(64, 1)
+  CS_ATTN_CASE(64, 2)
+  CS_ATTN_CASE(64, 4)
+  CS_ATTN_CASE(128, 1)
+  CS_ATTN_CASE(128, 2)
+  CS_ATTN_CASE(128, 4)
+  CS_ATTN_CASE(128, 5)
+  CS_ATTN_CASE(128, 8)
+#undef CS_ATTN_CASE
+  return false;
+}
+
+}  // namespace csk

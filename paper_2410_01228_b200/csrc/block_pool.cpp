@@ -68,6 +68,7 @@ Req* BlockPool::find_mut(int64_t id) {
 
 // ------------------------------------------------------------ physical ----
 int32_t BlockPool::take_block() {
+  if (free_blocks_.empty()) reclaim();
   if (free_blocks_.empty()) {
     throw PoolError("physical KV block pool exhausted (byte accounting fit; raise extra_blocks)");
   }
@@ -77,6 +78,7 @@ int32_t BlockPool::take_block() {
 }
 
 int32_t BlockPool::take_slot() {
+  if (free_slots_.empty()) reclaim();
   if (free_slots_.empty()) {
     throw PoolError("host slot pool exhausted (byte accounting fit; raise extra_host_slots)");
   }
@@ -108,7 +110,7 @@ bool BlockPool::job_prefix_done(int32_t dir, int64_t tag) const {
 // completed (a gather may still be reading it, a restore may be writing it).
 void BlockPool::reclaim() {
   auto keep_b = std::stable_partition(block_q_.begin(), block_q_.end(), [&](const Quarantined& q) {
-    return !(fwd_completed_ >= q.fwd_tag + 1 && job_prefix_done(CS_D2H, q.d2h_tag) &&
+    return !((!cfg_.fwd_quarantine || fwd_completed_ >= q.fwd_tag + 1) && job_prefix_done(CS_D2H, q.d2h_tag) &&
              job_prefix_done(CS_H2D, q.h2d_tag));
   });
   for (auto it = keep_b; it != block_q_.end(); ++it) free_blocks_.push_back(it->id);

@@ -79,6 +79,7 @@ struct PoolConfig {
   int64_t n_blocks = 0;             // physical blocks
   int64_t n_slots = 0;              // physical host slots
   int64_t moved_bytes_per_token = 0;  // this rank's bytes per token (shard)
+  bool fwd_quarantine = true;         // freed blocks wait for the next forward
 };
 
 struct Growth {  // uncommitted allocation segment (kv_cache.hpp:206-212)

@@ -1,0 +1,135 @@
+// Shared device helpers and the per-iteration descriptor layout.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace csk {
+
+// Per-iteration counts. Written by the host (H2D) before the forward; the
+// safepoint kernel truncates the *_cur fields in place to the online prefix
+// when the preemption flag carries this iteration's epoch.
+// Every kernel reads the *_cur counts, so a drop takes effect at the next
+// launch on the stream without host involvement.
+struct IterDesc {
+  int32_t n_tok_cur, n_tok_all, n_tok_on;      // token rows (GEMM M)
+  int32_t n_ent_cur, n_ent_all, n_ent_on;      // plan entries
+  int32_t n_dec_cur, n_dec_all, n_dec_on;      // single-query attention rows
+  int32_t n_pt_cur, n_pt_all, n_pt_on;         // prefill attention tiles
+  int32_t dropped_at;                          // layer of the drop, -1 if none
+  int32_t pad0;
+  uint64_t epoch;
+  uint64_t drop_ns;                            // %globaltimer at the drop
+};
+
+// Mapped (zero-copy) host<->device record for the preemption handshake.
+struct PreemptMailbox {
+  volatile uint64_t flag_epoch;      // host writes the epoch to preempt
+  volatile uint64_t flag_host_ns;    // host CLOCK_MONOTONIC at the store
+  volatile int32_t seen_layer;       // device: layer of the observed drop
+  volatile int32_t pad;
+  volatile uint64_t seen_epoch;      // device: epoch it dropped
+  volatile uint64_t seen_gpu_ns;     // device %globaltimer at the drop
+};
+
+// Prefill tile: TILE_ROWS query rows (token, head-in-group) of one entry.
+struct PrefillTile {
+  int32_t entry;
+  int32_t row0;      // first packed row (token_local * G + h) within the entry
+};
+
+// Up to 3 (local_start, global_start) row segments: maps a rank's rows of a
+// sharded weight onto the global tensor (q|k|v or gate|up blocks).
+struct RowMap {
+  int32_t n;
+  int32_t local_start[3];
+  int64_t global_start[3];
+};
+
+struct AttnParams {
+  const __nv_bfloat16* qkv;     // [T, (Hq + 2 Hkv) * D] rank-local heads
+  __nv_bfloat16* out;           // [T, Hq * D]
+  const __nv_bfloat16* pool;    // KV pool [blocks][L][2][Hkv][16][D]
+  const IterDesc* desc;
+  const int32_t* tok_pos;       // [T]
+  const int32_t* ent_q0;        // [E] first token row of the entry
+  const int32_t* ent_qlen;      // [E]
+  const int32_t* ent_kvlen;     // [E]
+  const int32_t* ent_bt;        // [E] offset into block_table
+  const int32_t* block_table;   // flat
+  const int32_t* dec_ent;       // [n_dec] entry index of single-query entries
+  const PrefillTile* tiles;     // [n_pt]
+  float* ws;                    // split-K partials
+  int32_t layer, num_layers, hq, hkv, qkv_stride;
+  int32_t n_splits, pages_per_split;
+  float scale_log2;             // softmax_scale * log2(e)
+};
+
+__host__ __device__ inline uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// Teacher-forced synthetic token id: id(req,pos).
+__host__ __device__ inline int32_t token_id(uint64_t seed, int64_t req, int64_t pos, int32_t vocab) {
+  uint64_t h = mix64(seed ^ mix64(static_cast<uint64_t>(req) * 0x100000001b3ULL + static_cast<uint64_t>(pos)));
+  return static_cast<int32_t>(h % static_cast<uint64_t>(vocab));
+}
+
+// Uniform in [-1, 1) from (seed, tensor, index); used for random-init weights.
+__host__ __device__ inline float hash_uniform(uint64_t seed, uint64_t tensor, uint64_t idx) {
+  uint64_t h = mix64(seed ^ mix64(tensor * 0x9E3779B97F4A7C15ULL ^ mix64(idx)));
+  return static_cast<float>(static_cast<int64_t>(h >> 40) - (1LL << 23)) * (1.0f / 8388608.0f);
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void ldmatrix_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
+  uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(s));
+}
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3,
+                                                  const void* p) {
+  uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(s));
+}
+
+// D = A(16x16 bf16, row) * B(16x8 bf16, col) + D (fp32)
+__device__ __forceinline__ void mma_bf16_16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Byte offset of 16-byte chunk c of row r in a [rows][D] bf16 tile stored
+// with an XOR swizzle over 8-chunk groups (conflict-free ldmatrix).
+template <int D>
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+  return static_cast<uint32_t>(r * (D * 2) + ((c ^ (r & 7)) << 4));
+}
+
+}  // namespace csk

@@ -1,0 +1,1200 @@
+// cs_engine: the C-ABI (include/conserve_b200.h) over the block pool, the
+// layer forward and the checkpoint/restore data movement.
+//
+// Streams: compute (forward), d2h (checkpoint gather), h2d (restore). The
+// forward is enqueued layer by layer; when the iteration carries offline work
+// and the policy is instrumented, a worker thread paces the enqueue
+// `layer_lookahead` layers ahead of the device so the host can shrink the
+// GEMM M dimension once a preemption flag is seen, while the device-side
+// safepoint kernel truncates every other kernel at the layer boundary itself.
+#include <cublas_v2.h>
+#include <nccl.h>
+#include <time.h>
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/conserve_b200.h"
+#include "block_pool.h"
+#include "common.cuh"
+
+namespace csk {
+void init_matrix(__nv_bfloat16* w, int64_t rows, int64_t cols, int64_t global_cols, int64_t col_off,
+                 const RowMap& map, uint64_t seed, uint64_t tensor, float scale, float offset, cudaStream_t s);
+void embed(__nv_bfloat16* x, const __nv_bfloat16* emb, const int32_t* tok_ids, int hidden, const IterDesc* desc,
+           int grid, cudaStream_t s);
+void add_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16* w, __nv_bfloat16* xn, int hidden,
+                 float eps, const IterDesc* desc, const int32_t* row_idx, int grid, cudaStream_t s);
+void silu_mul(const __nv_bfloat16* gu, __nv_bfloat16* act, int ffn, const IterDesc* desc, int grid_rows,
+              cudaStream_t s);
+void rope_append(__nv_bfloat16* qkv, const int32_t* tok_pos, const int32_t* tok_slot, __nv_bfloat16* pool, int hq,
+                 int hkv, int D, int num_layers, int layer, float theta, const IterDesc* desc, int grid,
+                 cudaStream_t s);
+void argmax_rows(const float* logits, int vocab, int32_t* out, const IterDesc* desc, int grid, cudaStream_t s);
+void safepoint(IterDesc* desc, PreemptMailbox* mb, int layer, cudaStream_t s);
+void safepoint_vote(__nv_bfloat16* tail, const IterDesc* desc, const PreemptMailbox* mb, cudaStream_t s);
+void safepoint_agreed(IterDesc* desc, PreemptMailbox* mb, const __nv_bfloat16* tail, int layer, cudaStream_t s);
+void read_globaltimer(uint64_t* mapped_out, cudaStream_t s);
+void calib_clock(volatile uint64_t* mb, cudaStream_t s);
+void kv_move(bool to_host, __nv_bfloat16* pool, __nv_bfloat16* host_mapped, const void* segs_mapped, int n_segs,
+             int runs_per_seg, int D, int sms, cudaStream_t s);
+void fill_pool(__nv_bfloat16* pool, size_t n, uint64_t seed, cudaStream_t s);
+bool launch_attention(const AttnParams& p, int head_dim, int group, int n_dec_grid, int n_pt_grid, cudaStream_t s);
+}  // namespace csk
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_) + " @" + std::to_string(__LINE__)); \
+  } while (0)
+#define CKB(x)                                                                                  \
+  do {                                                                                          \
+    cublasStatus_t s_ = (x);                                                                    \
+    if (s_ != CUBLAS_STATUS_SUCCESS)                                                            \
+      throw CudaError(std::string(#x) + ": cublas status " + std::to_string(static_cast<int>(s_))); \
+  } while (0)
+#define CKN(x)                                                                                  \
+  do {                                                                                          \
+    ncclResult_t r_ = (x);                                                                      \
+    if (r_ != ncclSuccess) throw CudaError(std::string(#x) + ": " + ncclGetErrorString(r_));    \
+  } while (0)
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return CS_OK;
+  } catch (const csb::PoolError& e) {
+    g_err = e.what();
+    return CS_ERR_POOL;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return CS_ERR_CUDA;
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    return CS_ERR_CONFIG;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return CS_ERR_INVALID;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return CS_ERR_LOGIC;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return CS_ERR_RUNTIME;
+  }
+}
+
+uint64_t host_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return static_cast<uint64_t>(ts.tv_sec) * 1000000000ull + static_cast<uint64_t>(ts.tv_nsec);
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Shared ownership of a job's event pair: the descriptor ring and the job
+// record may release it in either order.
+struct EventPair {
+  cudaEvent_t start = nullptr, end = nullptr;
+  EventPair() {
+    CK(cudaEventCreate(&start));
+    CK(cudaEventCreate(&end));
+  }
+  ~EventPair() {
+    cudaEventDestroy(start);
+    cudaEventDestroy(end);
+  }
+};
+
+// Pinned, device-mapped FIFO ring for per-job segment descriptors; the move
+// kernel reads them over the host link directly (no extra H2D copy).
+struct DescRing {
+  uint8_t* host = nullptr;
+  uint8_t* dev = nullptr;
+  size_t cap = 0, head = 0;
+  struct Live {
+    size_t off, len;
+    std::shared_ptr<EventPair> ev;
+  };
+  std::deque<Live> live;
+  size_t alloc(size_t n, const std::shared_ptr<EventPair>& ev) {
+    if (n > cap) throw std::runtime_error("descriptor ring too small for one job");
+    if (head + n > cap) head = 0;
+    auto overlaps = [&](const Live& l) { return head < l.off + l.len && l.off < head + n; };
+    while (!live.empty() && std::any_of(live.begin(), live.end(), overlaps)) {
+      CK(cudaEventSynchronize(live.front().ev->end));
+      live.pop_front();
+    }
+    const size_t off = head;
+    live.push_back({off, n, ev});
+    head += align_up(n, 256);
+    return off;
+  }
+};
+
+}  // namespace
+
+struct cs_engine;
+
+namespace {
+
+struct DeviceMover : csb::Mover {
+  cs_engine* e;
+  struct Rec {
+    std::shared_ptr<EventPair> ev;
+    int dir;
+    int64_t bytes;
+    bool timed = false;
+  };
+  std::map<int64_t, Rec> recs;
+  explicit DeviceMover(cs_engine* eng) : e(eng) {}
+  void launch(int dir, int64_t job_id, const std::vector<csb::Segment>& segs);
+  void gather_to_host(int64_t job_id, const std::vector<csb::Segment>& segs) override { launch(CS_D2H, job_id, segs); }
+  void scatter_from_host(int64_t job_id, const std::vector<csb::Segment>& segs) override {
+    launch(CS_H2D, job_id, segs);
+  }
+  void wait_job(int64_t job_id) override;
+  void release_job(int64_t job_id) override { recs.erase(job_id); }
+};
+
+}  // namespace
+
+struct Weights {
+  __nv_bfloat16 *emb = nullptr, *final_norm = nullptr, *lm_head = nullptr;
+  std::vector<__nv_bfloat16*> attn_norm, mlp_norm, wqkv, wo, wgu, wd;
+};
+
+struct cs_engine {
+  cs_config cfg{};
+  bool host_only = false, no_model = false;
+  int L = 0, hidden = 0, hq = 0, hkv = 0, D = 0, ffn = 0, vocab = 0, G = 0, tp = 1, rank = 0;
+  int64_t block_elems = 0;  // per rank, all layers
+  int64_t max_tok = 0, max_ent = 0;
+  int sms = 148;
+
+  std::unique_ptr<csb::BlockPool> pool;
+  std::unique_ptr<DeviceMover> mover;
+
+  // device memory
+  __nv_bfloat16* kv = nullptr;
+  __nv_bfloat16* host_kv = nullptr;      // pinned
+  __nv_bfloat16* host_kv_dev = nullptr;  // mapped alias
+  void* weight_mem = nullptr;
+  Weights w;
+  __nv_bfloat16 *x = nullptr, *xn = nullptr, *qkv = nullptr, *attn = nullptr, *tmp = nullptr, *gu = nullptr,
+                *act = nullptr, *xl = nullptr;
+  float* logits = nullptr;
+  float* ws = nullptr;
+  size_t ws_floats = 0;
+  uint8_t* d_meta = nullptr;
+  uint8_t* h_meta = nullptr;
+  size_t meta_cap = 0;
+  uint8_t* d_out = nullptr;  // IterDesc + out ids
+  uint8_t* h_out = nullptr;
+  csk::PreemptMailbox* mailbox = nullptr;  // mapped pinned
+  csk::PreemptMailbox* mailbox_dev = nullptr;
+  int64_t clock_offset_ns = 0;  // gpu globaltimer - host CLOCK_MONOTONIC
+
+  cudaStream_t s_compute = nullptr, s_d2h = nullptr, s_h2d = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_fwd_done = nullptr;
+  std::vector<cudaEvent_t> ev_layer;
+  bool any_forward = false;
+  cublasHandle_t blas = nullptr;
+  void* blas_ws = nullptr;
+  ncclComm_t comm = nullptr;
+  DescRing ring[2];
+  double moved_ms[2] = {0, 0};
+
+  // iteration state
+  struct Iter {
+    bool active = false;
+    uint64_t epoch = 0;
+    int n_tok = 0, n_tok_on = 0, n_ent = 0, n_ent_on = 0, n_dec = 0, n_pt = 0;
+    bool has_offline = false, paced = false;
+    int splits = 1, pps = 1;
+    std::vector<cs_batch_entry> entries;
+    std::vector<std::array<int64_t, 3>> writes;  // (id, w0, w1) per entry (w0<0: none)
+    csk::AttnParams ap{};
+    const int32_t* d_tok_ids = nullptr;
+    const int32_t* d_tok_slot = nullptr;
+    const int32_t* d_ent_last = nullptr;
+    int gemm_trunc_layer = -1;
+    uint64_t signal_ns = 0;
+  } it;
+
+  // pacing worker
+  std::thread worker;
+  std::mutex mu;
+  std::condition_variable cv;
+  bool job_ready = false, job_done = true, quit = false;
+  std::string worker_err;
+
+  int64_t layer_gemm_rows(int layer);
+  void enqueue_layers();
+  void gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
+  void allreduce(__nv_bfloat16* buf, int64_t count);
+};
+
+namespace {
+
+void DeviceMover::launch(int dir, int64_t job_id, const std::vector<csb::Segment>& segs) {
+  Rec r;
+  r.ev = std::make_shared<EventPair>();
+  r.dir = dir;
+  r.bytes = 0;
+  const size_t n = segs.size() * sizeof(csb::Segment);
+  DescRing& ring = e->ring[dir];
+  const size_t off = ring.alloc(n, r.ev);
+  std::memcpy(ring.host + off, segs.data(), n);
+  cudaStream_t st = dir == CS_D2H ? e->s_d2h : e->s_h2d;
+  if (dir == CS_D2H && e->any_forward) CK(cudaStreamWaitEvent(st, e->ev_fwd_done, 0));
+  CK(cudaEventRecord(r.ev->start, st));
+  csk::kv_move(dir == CS_D2H, e->kv, e->host_kv_dev, ring.dev + off, static_cast<int>(segs.size()),
+               e->L * 2 * e->hkv, e->D, e->sms, st);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(r.ev->end, st));
+  recs.emplace(job_id, std::move(r));
+}
+
+void DeviceMover::wait_job(int64_t job_id) {
+  auto it = recs.find(job_id);
+  if (it == recs.end()) return;
+  CK(cudaEventSynchronize(it->second.ev->end));
+  if (!it->second.timed) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, it->second.ev->start, it->second.ev->end));
+    e->moved_ms[it->second.dir] += ms;
+    it->second.timed = true;
+  }
+}
+
+constexpr uint64_t kTensorEmb = 1, kTensorLm = 2, kTensorFinalNorm = 3;
+uint64_t tensor_id(int layer, int which) { return 1000ull + static_cast<uint64_t>(layer) * 16 + which; }
+enum { kWAttnNorm = 0, kWQkv = 1, kWO = 2, kWMlpNorm = 3, kWGu = 4, kWD = 5 };
+
+void validate(const cs_config& c) {
+  if (c.page_tokens != 16) throw ConfigError("page_tokens is fixed at 16");
+  if (c.num_layers < 1) throw ConfigError("num_layers must be >= 1");
+  if (c.safepoint_interval_layers < 1) throw ConfigError("safepoint_interval_layers must be >= 1");
+  if (c.tp_size < 1 || c.tp_rank < 0 || c.tp_rank >= c.tp_size) throw ConfigError("bad tp_rank/tp_size");
+  if (c.n_kv_heads % c.tp_size || c.n_heads % c.tp_size || c.ffn % c.tp_size)
+    throw ConfigError("heads and ffn must divide by tp_size (KV-head-group sharding)");
+  if (c.n_heads % c.n_kv_heads) throw ConfigError("n_heads must be a multiple of n_kv_heads");
+  if (c.head_dim != 64 && c.head_dim != 128) throw ConfigError("head_dim must be 64 or 128");
+  if (c.hidden % 8 || (c.ffn / c.tp_size) % 8) throw ConfigError("hidden and ffn shard must be multiples of 8");
+  const int64_t model_bpt = 2LL * c.num_layers * c.n_kv_heads * c.head_dim * 2;
+  if (c.kv_bytes_per_token != model_bpt)
+    throw ConfigError("kv_bytes_per_token must equal 2*L*H_kv*d*2 = " + std::to_string(model_bpt));
+  if (c.gpu_kv_capacity < 1 || c.host_kv_capacity < 1) throw ConfigError("KV capacities must be positive");
+  if (c.d2h_bandwidth <= 0 || c.h2d_bandwidth <= 0) throw ConfigError("transfer bandwidths must be positive");
+  if (c.max_batched_tokens < 1) throw ConfigError("max_batched_tokens must be >= 1");
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ GEMM ----
+// Row-major Y[M,N] = X[M,K] * W[N,K]^T on cuBLAS (plain library GEMM).
+void cs_engine::gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32) {
+  if (M <= 0) return;
+  const float alpha = 1.f, beta = 0.f;
+  CKB(cublasGemmEx(blas, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, W, CUDA_R_16BF, K, A, CUDA_R_16BF, K, &beta, C,
+                   out_f32 ? CUDA_R_32F : CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
+}
+
+void cs_engine::allreduce(__nv_bfloat16* buf, int64_t count) {
+  if (tp <= 1 || count <= 0) return;
+  CKN(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclBfloat16, ncclSum, comm, s_compute));
+}
+
+// GEMM rows for a layer: all token rows until the host has observed a drop.
+// Tokens are ordered online-first, so truncation is a prefix of the rows.
+int64_t cs_engine::layer_gemm_rows(int layer) {
+  if (it.gemm_trunc_layer >= 0 && layer >= it.gemm_trunc_layer) return it.n_tok_on;
+  return it.n_tok;
+}
+
+// Enqueues every layer of the current iteration (caller or worker thread).
+void cs_engine::enqueue_layers() {
+  const auto* desc = reinterpret_cast<const csk::IterDesc*>(d_meta);
+  auto* desc_mut = reinterpret_cast<csk::IterDesc*>(d_meta);
+  const int lookahead = cfg.layer_lookahead > 0 ? cfg.layer_lookahead : 2;
+  const bool instrumented = cfg.instrumented != 0 && it.has_offline;
+  const int qkv_cols = (hq + 2 * hkv) * D;
+  const int T = it.n_tok;
+  __nv_bfloat16* tail = tmp + static_cast<size_t>(max_tok) * hidden;  // vote slot
+  auto is_sp = [&](int l) { return instrumented && l > 0 && l < L && l % cfg.safepoint_interval_layers == 0; };
+
+  for (int l = 0; l < L; ++l) {
+    if (it.paced && l > lookahead) CK(cudaEventSynchronize(ev_layer[l - lookahead - 1]));
+    if (is_sp(l)) {
+      // Host view of the flag: once seen, later layers' GEMMs shrink to the
+      // online rows (the device truncates everything else at this layer).
+      if (tp == 1) {
+        if (it.gemm_trunc_layer < 0 && mailbox->flag_epoch == it.epoch) it.gemm_trunc_layer = l;
+      } else if (it.gemm_trunc_layer < 0 && mailbox->seen_epoch == it.epoch && mailbox->seen_layer >= 0 &&
+                 mailbox->seen_layer <= l - lookahead - 1) {
+        // TP: follow the device-agreed drop layer, deterministic on all ranks.
+        it.gemm_trunc_layer = l;
+      }
+    }
+    const int64_t M = layer_gemm_rows(l);
+    if (l == 0) {
+      csk::embed(x, w.emb, it.d_tok_ids, hidden, desc, T, s_compute);
+    }
+    if (is_sp(l)) {
+      if (tp == 1) {
+        csk::safepoint(desc_mut, mailbox_dev, l, s_compute);
+      } else {
+        csk::safepoint_agreed(desc_mut, mailbox_dev, tail, l, s_compute);
+      }
+    }
+    csk::add_rmsnorm(x, l == 0 ? nullptr : tmp, w.attn_norm[l], xn, hidden, cfg.rms_eps, desc, nullptr, T, s_compute);
+    gemm(xn, w.wqkv[l], qkv, static_cast<int>(M), qkv_cols, hidden, false);
+    csk::rope_append(qkv, it.ap.tok_pos, it.d_tok_slot, kv, hq, hkv, D, L, l,
+                     cfg.rope_theta, desc, T, s_compute);
+    csk::AttnParams ap = it.ap;
+    ap.layer = l;
+    if (!csk::launch_attention(ap, D, G, it.n_dec, it.n_pt, s_compute))
+      throw ConfigError("unsupported attention shape");
+    gemm(attn, w.wo[l], tmp, static_cast<int>(M), hidden, hq * D, false);
+    allreduce(tmp, M * hidden);
+    csk::add_rmsnorm(x, tmp, w.mlp_norm[l], xn, hidden, cfg.rms_eps, desc, nullptr, T, s_compute);
+    gemm(xn, w.wgu[l], gu, static_cast<int>(M), 2 * ffn, hidden, false);
+    csk::silu_mul(gu, act, ffn, desc, T, s_compute);
+    gemm(act, w.wd[l], tmp, static_cast<int>(M), hidden, ffn, false);
+    if (tp > 1) {
+      if (is_sp(l + 1)) {
+        csk::safepoint_vote(tmp + M * hidden, desc, mailbox_dev, s_compute);
+        allreduce(tmp, M * hidden + 8);
+        CK(cudaMemcpyAsync(tail, tmp + M * hidden, 16, cudaMemcpyDeviceToDevice, s_compute));
+      } else {
+        allreduce(tmp, M * hidden);
+      }
+    }
+    if (it.paced) CK(cudaEventRecord(ev_layer[l], s_compute));
+    if (cfg.flags & CS_FLAG_SYNC_DEBUG) {
+      CK(cudaStreamSynchronize(s_compute));
+      CK(cudaGetLastError());
+    }
+  }
+  // Final norm of each entry's last row -> lm_head -> argmax.
+  const int E = it.n_ent;
+  csk::add_rmsnorm(x, tmp, w.final_norm, xl, hidden, cfg.rms_eps, desc, it.d_ent_last, E, s_compute);
+  gemm(xl, w.lm_head, logits, E, vocab, hidden, true);
+  csk::argmax_rows(logits, vocab, reinterpret_cast<int32_t*>(d_out + sizeof(csk::IterDesc)), desc, E, s_compute);
+  CK(cudaMemcpyAsync(d_out, d_meta, sizeof(csk::IterDesc), cudaMemcpyDeviceToDevice, s_compute));
+  CK(cudaMemcpyAsync(h_out, d_out, sizeof(csk::IterDesc) + sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s_compute));
+  CK(cudaEventRecord(ev_end, s_compute));
+  CK(cudaEventRecord(ev_fwd_done, s_compute));
+  CK(cudaGetLastError());
+}
+
+extern "C" {
+
+const char* cs_last_error(void) { return g_err.c_str(); }
+const char* cs_version(void) { return "conserve_b200 0.1 (sm_100a)"; }
+
+void cs_config_default(cs_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  // tiny config-1 decoder: 2 layers, d_model 256, 4 heads
+  c->num_layers = 2;
+  c->hidden = 256;
+  c->n_heads = 4;
+  c->n_kv_heads = 4;
+  c->head_dim = 64;
+  c->ffn = 512;
+  c->vocab = 1024;
+  c->rope_theta = 10000.f;
+  c->rms_eps = 1e-5f;
+  c->weight_seed = 1;
+  c->token_seed = 1;
+  c->kv_bytes_per_token = 2048;
+  c->gpu_kv_capacity = 64LL * 16 * 2048;
+  c->host_kv_capacity = 4096LL * 16 * 2048;
+  c->d2h_bandwidth = 38797312000.0;
+  c->h2d_bandwidth = 38797312000.0;
+  c->gather_cost_us = 500.0;
+  c->page_tokens = 16;
+  c->safepoint_interval_layers = 1;
+  c->max_batched_tokens = 512;
+  c->incremental = 1;
+  c->instrumented = 1;
+  c->extra_blocks = -1;
+  c->extra_host_slots = -1;
+  c->max_entries = 0;
+  c->layer_lookahead = 0;
+  c->tp_rank = 0;
+  c->tp_size = 1;
+  c->device = 0;
+  c->flags = 0;
+}
+
+int cs_create(const cs_config* cfg, cs_engine** out) {
+  return guard([&] {
+    validate(*cfg);
+    auto e = std::make_unique<cs_engine>();
+    e->cfg = *cfg;
+    e->host_only = (cfg->flags & CS_FLAG_HOST_ONLY) != 0;
+    e->no_model = (cfg->flags & CS_FLAG_NO_MODEL) != 0;
+    e->tp = cfg->tp_size;
+    e->rank = cfg->tp_rank;
+    e->L = cfg->num_layers;
+    e->hidden = cfg->hidden;
+    e->hq = cfg->n_heads / cfg->tp_size;
+    e->hkv = cfg->n_kv_heads / cfg->tp_size;
+    e->G = cfg->n_heads / cfg->n_kv_heads;
+    e->D = cfg->head_dim;
+    e->ffn = cfg->ffn / cfg->tp_size;
+    e->vocab = cfg->vocab;
+    e->block_elems = static_cast<int64_t>(e->L) * 2 * e->hkv * 16 * e->D;
+    e->max_tok = cfg->max_batched_tokens;
+    e->max_ent = cfg->max_entries > 0 ? cfg->max_entries : 1024;
+
+    const int64_t page_bytes = 16LL * cfg->kv_bytes_per_token;
+    const int64_t base_blocks = (cfg->gpu_kv_capacity + page_bytes - 1) / page_bytes;
+    const int64_t extra_b = cfg->extra_blocks >= 0 ? cfg->extra_blocks
+                                                   : 2 * (e->max_tok / 16 + e->max_ent) + 64;
+    const int64_t base_slots = (cfg->host_kv_capacity + page_bytes - 1) / page_bytes;
+    const int64_t extra_s = cfg->extra_host_slots >= 0 ? cfg->extra_host_slots : e->max_ent + 64;
+
+    csb::PoolConfig pc;
+    pc.page_tokens = 16;
+    pc.kv_bytes_per_token = cfg->kv_bytes_per_token;
+    pc.gpu_capacity = cfg->gpu_kv_capacity;
+    pc.host_capacity = cfg->host_kv_capacity;
+    pc.d2h_bw = cfg->d2h_bandwidth;
+    pc.h2d_bw = cfg->h2d_bandwidth;
+    pc.gather_us = cfg->gather_cost_us;
+    pc.incremental = cfg->incremental != 0;
+    pc.n_blocks = base_blocks + extra_b;
+    pc.n_slots = base_slots + extra_s;
+    pc.moved_bytes_per_token = cfg->kv_bytes_per_token / cfg->tp_size;
+    pc.fwd_quarantine = (cfg->flags & CS_FLAG_NO_FWD_QUARANTINE) == 0;
+
+    if (!e->host_only) {
+      CK(cudaSetDevice(cfg->device));
+      CK(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, cfg->device));
+      CK(cudaStreamCreateWithFlags(&e->s_compute, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&e->s_d2h, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&e->s_h2d, cudaStreamNonBlocking));
+      CK(cudaEventCreate(&e->ev_start));
+      CK(cudaEventCreate(&e->ev_end));
+      CK(cudaEventCreateWithFlags(&e->ev_fwd_done, cudaEventDisableTiming));
+      e->ev_layer.resize(static_cast<size_t>(e->L));
+      for (auto& ev : e->ev_layer) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+
+      const size_t blk_bytes = static_cast<size_t>(e->block_elems) * 2;
+      CK(cudaMalloc(&e->kv, static_cast<size_t>(pc.n_blocks) * blk_bytes));
+      CK(cudaHostAlloc(&e->host_kv, static_cast<size_t>(pc.n_slots) * blk_bytes,
+                       cudaHostAllocMapped | cudaHostAllocPortable));
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->host_kv_dev), e->host_kv, 0));
+      for (int d = 0; d < 2; ++d) {
+        e->ring[d].cap = 8u << 20;
+        CK(cudaHostAlloc(&e->ring[d].host, e->ring[d].cap, cudaHostAllocMapped | cudaHostAllocPortable));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->ring[d].dev), e->ring[d].host, 0));
+      }
+      CK(cudaHostAlloc(&e->mailbox, sizeof(csk::PreemptMailbox), cudaHostAllocMapped | cudaHostAllocPortable));
+      std::memset(e->mailbox, 0, sizeof(csk::PreemptMailbox));
+      e->mailbox->seen_layer = -1;
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->mailbox_dev), e->mailbox, 0));
+      e->mover = std::make_unique<DeviceMover>(e.get());
+
+      if (!e->no_model) {
+        // weights, one allocation
+        const int64_t H = e->hidden, qkv_rows = static_cast<int64_t>(e->hq + 2 * e->hkv) * e->D;
+        const int64_t per_layer = 2 * H + qkv_rows * H + H * e->hq * e->D + 2LL * e->ffn * H + H * e->ffn;
+        const int64_t total = 2LL * e->vocab * H + H + per_layer * e->L;
+        CK(cudaMalloc(&e->weight_mem, static_cast<size_t>(total) * 2));
+        __nv_bfloat16* p = static_cast<__nv_bfloat16*>(e->weight_mem);
+        auto take = [&](int64_t n) {
+          __nv_bfloat16* r = p;
+          p += n;
+          return r;
+        };
+        e->w.emb = take(e->vocab * H);
+        e->w.lm_head = take(e->vocab * H);
+        e->w.final_norm = take(H);
+        const uint64_t seed = cfg->weight_seed;
+        const float wscale = 0.02f * 1.7320508f;  // uniform with std 0.02
+        csk::RowMap ident{1, {0, 0, 0}, {0, 0, 0}};
+        cudaStream_t s = e->s_compute;
+        csk::init_matrix(e->w.emb, e->vocab, H, H, 0, ident, seed, kTensorEmb, wscale, 0.f, s);
+        csk::init_matrix(e->w.lm_head, e->vocab, H, H, 0, ident, seed, kTensorLm, wscale, 0.f, s);
+        csk::init_matrix(e->w.final_norm, 1, H, H, 0, ident, seed, kTensorFinalNorm, 0.1f, 1.f, s);
+        const int64_t Hq_g = cfg->n_heads, Hkv_g = cfg->n_kv_heads, F_g = cfg->ffn;
+        for (int l = 0; l < e->L; ++l) {
+          e->w.attn_norm.push_back(take(H));
+          e->w.wqkv.push_back(take(qkv_rows * H));
+          e->w.wo.push_back(take(H * e->hq * e->D));
+          e->w.mlp_norm.push_back(take(H));
+          e->w.wgu.push_back(take(2LL * e->ffn * H));
+          e->w.wd.push_back(take(H * e->ffn));
+          csk::init_matrix(e->w.attn_norm[l], 1, H, H, 0, ident, seed, tensor_id(l, kWAttnNorm), 0.1f, 1.f, s);
+          csk::init_matrix(e->w.mlp_norm[l], 1, H, H, 0, ident, seed, tensor_id(l, kWMlpNorm), 0.1f, 1.f, s);
+          // qkv: global rows [q heads | k heads | v heads] x D; this rank's heads
+          csk::RowMap qkv_map{3,
+                              {0, e->hq * e->D, (e->hq + e->hkv) * e->D},
+                              {static_cast<int64_t>(e->rank) * e->hq * e->D,
+                               Hq_g * e->D + static_cast<int64_t>(e->rank) * e->hkv * e->D,
+                               (Hq_g + Hkv_g) * e->D + static_cast<int64_t>(e->rank) * e->hkv * e->D}};
+          csk::init_matrix(e->w.wqkv[l], qkv_rows, H, H, 0, qkv_map, seed, tensor_id(l, kWQkv), wscale, 0.f, s);
+          // o_proj: row-parallel -> this rank's input columns
+          csk::init_matrix(e->w.wo[l], H, e->hq * e->D, Hq_g * e->D, static_cast<int64_t>(e->rank) * e->hq * e->D,
+                           ident, seed, tensor_id(l, kWO), wscale, 0.f, s);
+          csk::RowMap gu_map{2, {0, e->ffn, 0}, {static_cast<int64_t>(e->rank) * e->ffn,
+                                                 F_g + static_cast<int64_t>(e->rank) * e->ffn, 0}};
+          csk::init_matrix(e->w.wgu[l], 2LL * e->ffn, H, H, 0, gu_map, seed, tensor_id(l, kWGu), wscale, 0.f, s);
+          csk::init_matrix(e->w.wd[l], H, e->ffn, F_g, static_cast<int64_t>(e->rank) * e->ffn, ident, seed,
+                           tensor_id(l, kWD), wscale, 0.f, s);
+        }
+        CK(cudaGetLastError());
+        // activations
+        const int64_t T = e->max_tok;
+        CK(cudaMalloc(&e->x, T * H * 2));
+        CK(cudaMalloc(&e->xn, T * H * 2));
+        CK(cudaMalloc(&e->qkv, T * qkv_rows * 2));
+        CK(cudaMalloc(&e->attn, T * e->hq * e->D * 2));
+        CK(cudaMalloc(&e->tmp, (T * H + 64) * 2));
+        CK(cudaMemset(e->tmp, 0, (T * H + 64) * 2));
+        CK(cudaMalloc(&e->gu, T * 2 * e->ffn * 2));
+        CK(cudaMalloc(&e->act, T * e->ffn * 2));
+        CK(cudaMalloc(&e->xl, e->max_ent * H * 2));
+        CK(cudaMalloc(&e->logits, static_cast<size_t>(e->max_ent) * e->vocab * 4));
+        CK(cudaMalloc(&e->d_out, sizeof(csk::IterDesc) + 4 * e->max_ent));
+        CK(cudaMallocHost(&e->h_out, sizeof(csk::IterDesc) + 4 * e->max_ent));
+        CKB(cublasCreate(&e->blas));
+        CKB(cublasSetStream(e->blas, e->s_compute));
+        CK(cudaMalloc(&e->blas_ws, 64u << 20));
+        CKB(cublasSetWorkspace(e->blas, e->blas_ws, 64u << 20));
+        CKB(cublasSetMathMode(e->blas, CUBLAS_DEFAULT_MATH));
+      }
+      CK(cudaStreamSynchronize(e->s_compute));
+      // globaltimer <-> CLOCK_MONOTONIC offset (preemption latency probe)
+      {
+        volatile uint64_t* mbx = reinterpret_cast<volatile uint64_t*>(const_cast<uint64_t*>(&e->mailbox->flag_host_ns));
+        int64_t best = INT64_MAX;
+        for (int rep = 0; rep < 5; ++rep) {
+          e->mailbox->flag_host_ns = 0;
+          e->mailbox->seen_gpu_ns = 0;
+          csk::calib_clock(reinterpret_cast<volatile uint64_t*>(e->mailbox_dev), e->s_compute);
+          struct timespec ts {0, 200000};
+          nanosleep(&ts, nullptr);
+          const uint64_t t0 = host_ns();
+          *mbx = t0;
+          while (e->mailbox->seen_gpu_ns == 0) {
+          }
+          const int64_t off = static_cast<int64_t>(e->mailbox->seen_gpu_ns) - static_cast<int64_t>(t0);
+          if (off < best || rep == 0) best = std::min(best, off);
+          CK(cudaStreamSynchronize(e->s_compute));
+        }
+        e->clock_offset_ns = best;
+        e->mailbox->flag_host_ns = 0;
+        e->mailbox->seen_gpu_ns = 0;
+        e->mailbox->seen_epoch = 0;
+        e->mailbox->seen_layer = -1;
+      }
+    }
+    e->pool = std::make_unique<csb::BlockPool>(pc, e->mover.get());
+    *out = e.release();
+  });
+}
+
+int cs_destroy(cs_engine* e) {
+  if (!e) return CS_OK;
+  return guard([&] {
+    {
+      std::lock_guard<std::mutex> lk(e->mu);
+      e->quit = true;
+    }
+    e->cv.notify_all();
+    if (e->worker.joinable()) e->worker.join();
+    if (!e->host_only) {
+      cudaDeviceSynchronize();
+      e->mover.reset();
+      for (auto& r : e->ring) r.live.clear();
+      if (e->blas) cublasDestroy(e->blas);
+      if (e->comm) ncclCommDestroy(e->comm);
+      cudaFree(e->kv);
+      cudaFreeHost(e->host_kv);
+      for (auto& r : e->ring) cudaFreeHost(r.host);
+      cudaFreeHost(e->mailbox);
+      cudaFree(e->weight_mem);
+      for (void* p : {static_cast<void*>(e->x), static_cast<void*>(e->xn), static_cast<void*>(e->qkv),
+                      static_cast<void*>(e->attn), static_cast<void*>(e->tmp), static_cast<void*>(e->gu),
+                      static_cast<void*>(e->act), static_cast<void*>(e->xl), static_cast<void*>(e->logits),
+                      static_cast<void*>(e->ws), static_cast<void*>(e->d_meta), static_cast<void*>(e->d_out),
+                      e->blas_ws})
+        if (p) cudaFree(p);
+      if (e->h_meta) cudaFreeHost(e->h_meta);
+      if (e->h_out) cudaFreeHost(e->h_out);
+      cudaEventDestroy(e->ev_start);
+      cudaEventDestroy(e->ev_end);
+      cudaEventDestroy(e->ev_fwd_done);
+      for (auto& ev : e->ev_layer) cudaEventDestroy(ev);
+      cudaStreamDestroy(e->s_compute);
+      cudaStreamDestroy(e->s_d2h);
+      cudaStreamDestroy(e->s_h2d);
+    }
+    delete e;
+  });
+}
+
+int cs_nccl_unique_id(uint8_t out_id[128]) {
+  return guard([&] {
+    ncclUniqueId id;
+    CKN(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "nccl id size");
+    std::memcpy(out_id, &id, 128);
+  });
+}
+
+int cs_nccl_init(cs_engine* e, const uint8_t id[128]) {
+  return guard([&] {
+    if (e->tp <= 1) return;
+    ncclUniqueId nid;
+    std::memcpy(&nid, id, 128);
+    CK(cudaSetDevice(e->cfg.device));
+    CKN(ncclCommInitRank(&e->comm, e->tp, nid, e->rank));
+  });
+}
+
+// ------------------------------------------------------------ KV pool API --
+int cs_kv_register_request(cs_engine* e, int64_t id, int32_t online) {
+  return guard([&] { e->pool->register_request(id, online != 0); });
+}
+int cs_kv_allocate(cs_engine* e, int64_t id, int64_t n, int64_t now, cs_alloc_result* out) {
+  (void)now;
+  return guard([&] { *out = e->pool->allocate(id, n); });
+}
+int cs_kv_commit(cs_engine* e, int64_t id) { return guard([&] { e->pool->commit(id); }); }
+int cs_kv_rollback(cs_engine* e, int64_t id) { return guard([&] { e->pool->rollback(id); }); }
+int cs_kv_evict_request_gpu(cs_engine* e, int64_t id, int64_t now, int64_t max_pages, cs_evict_stats* out) {
+  (void)now;
+  return guard([&] { *out = e->pool->evict_request_gpu(id, max_pages); });
+}
+int cs_kv_discard_request(cs_engine* e, int64_t id, int64_t now, cs_evict_stats* out) {
+  (void)now;
+  return guard([&] { *out = e->pool->discard_request(id); });
+}
+int cs_kv_release_offline_pages_on_demand(cs_engine* e, int64_t needed, int64_t now, int64_t* freed,
+                                          int64_t* discards, int64_t cap, int64_t* n_discards) {
+  (void)now;
+  return guard([&] {
+    csb::ReleaseResult r = e->pool->release_offline_pages_on_demand(needed);
+    *freed = r.freed_pages;
+    *n_discards = static_cast<int64_t>(r.discards.size());
+    for (size_t i = 0; i < r.discards.size() && static_cast<int64_t>(i) < cap; ++i) {
+      discards[2 * i] = r.discards[i].first;
+      discards[2 * i + 1] = r.discards[i].second;
+    }
+  });
+}
+int cs_kv_releasable_offline_pages_now(cs_engine* e, int64_t* out) {
+  return guard([&] { *out = e->pool->releasable_offline_pages_now(); });
+}
+int cs_kv_stage_checkpoint(cs_engine* e, int64_t id, int64_t from, int64_t to) {
+  return guard([&] { e->pool->stage_checkpoint(id, from, to); });
+}
+int cs_kv_flush_checkpoints(cs_engine* e, int64_t now, cs_transfer_job* job, int32_t* has_job) {
+  return guard([&] {
+    auto j = e->pool->flush_checkpoints(now);
+    *has_job = j.has_value() ? 1 : 0;
+    if (j) *job = *j;
+  });
+}
+int cs_kv_resume_cost(cs_engine* e, int64_t id, cs_resume_cost* out) {
+  return guard([&] { *out = e->pool->resume_cost(id); });
+}
+int cs_kv_fully_resident(cs_engine* e, int64_t id, int32_t* out) {
+  return guard([&] { *out = e->pool->fully_resident(id) ? 1 : 0; });
+}
+int cs_kv_prefetch_inflight(cs_engine* e, int64_t id, int32_t* out) {
+  return guard([&] { *out = e->pool->prefetch_inflight(id) ? 1 : 0; });
+}
+int cs_kv_start_prefetch(cs_engine* e, int64_t id, int64_t now, cs_transfer_job* job, int32_t* has_job) {
+  return guard([&] {
+    auto j = e->pool->start_prefetch(id, now);
+    *has_job = j.has_value() ? 1 : 0;
+    if (j) *job = *j;
+  });
+}
+int cs_kv_recompute_chunk(cs_engine* e, int64_t id, int64_t desired, int64_t cap, int64_t* out) {
+  return guard([&] { *out = e->pool->recompute_chunk(id, desired, cap); });
+}
+int cs_kv_on_transfer_done(cs_engine* e, int64_t job_id, int64_t now, cs_transfer_done* out) {
+  (void)now;
+  return guard([&] {
+    csb::DoneResult r = e->pool->on_transfer_done(job_id);
+    out->freed_pages = r.freed_pages;
+    out->n_became_resident = static_cast<int32_t>(r.became_resident.size());
+    for (size_t i = 0; i < r.became_resident.size() && i < 4; ++i) out->became_resident[i] = r.became_resident[i];
+  });
+}
+int cs_kv_on_request_paused(cs_engine* e, int64_t id, uint64_t seq) {
+  return guard([&] { e->pool->on_request_paused(id, seq); });
+}
+int cs_kv_on_request_active(cs_engine* e, int64_t id) { return guard([&] { e->pool->on_request_active(id); }); }
+int cs_kv_release_request(cs_engine* e, int64_t id) { return guard([&] { e->pool->release_request(id); }); }
+int cs_kv_note_written(cs_engine* e, int64_t id, int64_t w0, int64_t w1) {
+  return guard([&] { e->pool->note_written(id, w0, w1); });
+}
+int cs_kv_stats_get(cs_engine* e, cs_kv_stats* o) {
+  return guard([&] {
+    const csb::BlockPool& p = *e->pool;
+    o->gpu_used_bytes = p.gpu_used();
+    o->gpu_free_bytes = p.gpu_free();
+    o->host_used_bytes = p.host_used();
+    o->gpu_free_pages = p.gpu_free_pages();
+    o->page_bytes = p.page_bytes();
+    o->total_d2h_bytes = p.total_d2h();
+    o->total_h2d_bytes = p.total_h2d();
+    o->recompute_tagged_tokens = p.recompute_tagged();
+    o->transfers_inflight = p.transfers_inflight() ? 1 : 0;
+    o->n_blocks = p.n_blocks();
+    o->free_blocks = p.free_blocks();
+    o->quarantined_blocks = p.quarantined_blocks();
+    o->n_host_slots = p.n_slots();
+    o->free_host_slots = p.free_slots();
+    o->moved_d2h_bytes = p.moved_d2h();
+    o->moved_h2d_bytes = p.moved_h2d();
+    o->nonresident_reads = p.nonresident_reads();
+    o->moved_d2h_ms = e->moved_ms[CS_D2H];
+    o->moved_h2d_ms = e->moved_ms[CS_H2D];
+  });
+}
+int cs_kv_request_info(cs_engine* e, int64_t id, int64_t* gpu_pages, int64_t* covered, int64_t* pending) {
+  return guard([&] {
+    *gpu_pages = e->pool->request_gpu_pages(id);
+    *covered = e->pool->covered_tokens(id);
+    *pending = e->pool->pending_append_tokens(id);
+  });
+}
+int cs_kv_audit(cs_engine* e) { return guard([&] { e->pool->audit(); }); }
+int cs_kv_page_table_json(cs_engine* e, int64_t id, char* buf, size_t cap, size_t* len) {
+  return guard([&] {
+    const std::string s = e->pool->page_table_json(id);
+    *len = s.size();
+    if (buf && cap > 0) {
+      const size_t n = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+int cs_kv_block_table(cs_engine* e, int64_t id, int32_t* blocks, int32_t* slots, int64_t cap, int64_t* n) {
+  return guard([&] {
+    const csb::Req* r = e->pool->find(id);
+    if (!r) throw std::logic_error("unknown request id in kv manager");
+    *n = static_cast<int64_t>(r->pages.size());
+    for (int64_t i = 0; i < *n && i < cap; ++i) {
+      if (blocks) blocks[i] = r->pages[static_cast<size_t>(i)].block;
+      if (slots) slots[i] = r->pages[static_cast<size_t>(i)].slot;
+    }
+  });
+}
+
+// ---------------------------------------------------------------- forward --
+int cs_forward_launch(cs_engine* e, const cs_batch_entry* entries, int32_t n, uint64_t epoch) {
+  return guard([&] {
+    if (e->it.active) throw std::logic_error("iterations overlap on the device");
+    if (n < 1) throw std::invalid_argument("empty batch");
+    if (n > e->max_ent) throw std::invalid_argument("plan has more entries than max_entries");
+    auto& it = e->it;
+    it = cs_engine::Iter{};
+    it.epoch = epoch;
+    it.entries.assign(entries, entries + n);
+    csb::BlockPool& pool = *e->pool;
+
+    // ---- host metadata: positions per 0.11 ----
+    std::vector<int32_t> tok_ids, tok_pos, tok_slot, ent_q0(n), ent_qlen(n), ent_kvlen(n), ent_bt(n), ent_last(n);
+    std::vector<int32_t> dec_ent, bt;
+    std::vector<csk::PrefillTile> tiles;
+    bool seen_offline = false;
+    int n_tok_on = 0, n_ent_on = 0, n_dec_on = 0, n_pt_on = 0, max_dec_pages = 0;
+    for (int i = 0; i < n; ++i) {
+      const cs_batch_entry& be = entries[i];
+      if (be.online && seen_offline) throw std::invalid_argument("online entries must form a prefix of the plan");
+      if (!be.online) seen_offline = true;
+      const csb::Req* r = pool.find(be.request_id);
+      if (!r) throw std::logic_error("unknown request id in kv manager");
+      std::vector<int32_t> pos;
+      std::array<int64_t, 3> wr{be.request_id, -1, -1};
+      if (be.kind == CS_DECODE) {
+        if (be.compute_tokens != 1 || be.context_tokens < 1) throw std::invalid_argument("decode entry needs P=1, C>=1");
+        pos.push_back(static_cast<int32_t>(be.context_tokens - 1));
+        wr = {be.request_id, be.context_tokens - 1, be.context_tokens};
+      } else if (be.kind == CS_PREFILL) {
+        if (be.compute_tokens < 1) throw std::invalid_argument("prefill entry needs P>=1");
+        for (int64_t p = 0; p < be.compute_tokens; ++p) pos.push_back(static_cast<int32_t>(be.context_tokens + p));
+        wr = {be.request_id, be.context_tokens, be.context_tokens + be.compute_tokens};
+      } else if (be.kind == CS_RECOMPUTE) {
+        // Positions of the pages re-materialized by this build's allocation
+        // (kv_cache.cpp:76-107), page order; BatchEntry.C is context_len.
+        std::vector<size_t> pages;
+        for (const csb::Growth& g : r->growth)
+          if (g.was_discarded) pages.push_back(g.page);
+        std::sort(pages.begin(), pages.end());
+        for (size_t pg : pages)
+          for (int64_t t = 0; t < r->pages[pg].tokens; ++t) pos.push_back(static_cast<int32_t>(pg * 16 + t));
+        if (static_cast<int64_t>(pos.size()) != be.compute_tokens)
+          throw std::logic_error("recompute entry does not match the re-materialized pages");
+      } else {
+        throw std::invalid_argument("unknown entry kind");
+      }
+      const int kv_len = pos.back() + 1;
+      ent_q0[i] = static_cast<int32_t>(tok_pos.size());
+      ent_qlen[i] = static_cast<int32_t>(pos.size());
+      ent_kvlen[i] = kv_len;
+      ent_bt[i] = static_cast<int32_t>(bt.size());
+      const int n_pages = (kv_len + 15) / 16;
+      for (int pg = 0; pg < n_pages; ++pg) bt.push_back(pool.block_for_read(be.request_id, static_cast<size_t>(pg)));
+      for (int32_t p : pos) {
+        tok_ids.push_back(csk::token_id(e->cfg.token_seed, be.request_id, p, e->vocab));
+        tok_pos.push_back(p);
+        tok_slot.push_back(bt[static_cast<size_t>(ent_bt[i] + p / 16)] * 16 + (p % 16));
+      }
+      ent_last[i] = static_cast<int32_t>(tok_pos.size()) - 1;
+      if (pos.size() == 1) {
+        dec_ent.push_back(i);
+        max_dec_pages = std::max(max_dec_pages, n_pages);
+      } else {
+        const int rows = static_cast<int>(pos.size()) * e->G;
+        for (int r0 = 0; r0 < rows; r0 += 64) tiles.push_back({i, r0});
+      }
+      if (be.online) {
+        n_tok_on = static_cast<int>(tok_pos.size());
+        n_ent_on = i + 1;
+        n_dec_on = static_cast<int>(dec_ent.size());
+        n_pt_on = static_cast<int>(tiles.size());
+      }
+      it.writes.push_back(wr);
+    }
+    const int T = static_cast<int>(tok_pos.size());
+    if (T > e->max_tok) throw std::invalid_argument("plan exceeds max_batched_tokens");
+    it.n_tok = T;
+    it.n_tok_on = n_tok_on;
+    it.n_ent = n;
+    it.n_ent_on = n_ent_on;
+    it.n_dec = static_cast<int>(dec_ent.size());
+    it.n_pt = static_cast<int>(tiles.size());
+    it.has_offline = seen_offline;
+    pool.on_forward_launched();
+    if (e->host_only || e->no_model) {
+      it.active = true;
+      return;
+    }
+
+    // ---- pack metadata: [desc | tok_ids | tok_pos | tok_slot | ent x5 (cap max_ent) | dec | tiles | bt] ----
+    const size_t E = static_cast<size_t>(e->max_ent);
+    size_t off = 0;
+    auto region = [&](size_t bytes) {
+      const size_t o = off;
+      off = align_up(off + bytes, 16);
+      return o;
+    };
+    const size_t o_desc = region(sizeof(csk::IterDesc));
+    const size_t o_tok = region(sizeof(int32_t) * 3 * static_cast<size_t>(T));
+    const size_t o_ent = region(sizeof(int32_t) * 5 * E);
+    const size_t o_dec = region(sizeof(int32_t) * dec_ent.size() + 4);
+    const size_t o_tiles = region(sizeof(csk::PrefillTile) * tiles.size() + 8);
+    const size_t o_bt = region(sizeof(int32_t) * bt.size() + 4);
+    const size_t total = off;
+    if (total > e->meta_cap) {
+      if (e->d_meta) CK(cudaFree(e->d_meta));
+      if (e->h_meta) CK(cudaFreeHost(e->h_meta));
+      e->meta_cap = align_up(total * 2, 1 << 20);
+      CK(cudaMalloc(&e->d_meta, e->meta_cap));
+      CK(cudaMallocHost(&e->h_meta, e->meta_cap));
+    }
+    uint8_t* h = e->h_meta;
+    csk::IterDesc desc{};
+    desc.n_tok_cur = desc.n_tok_all = T;
+    desc.n_tok_on = n_tok_on;
+    desc.n_ent_cur = desc.n_ent_all = n;
+    desc.n_ent_on = n_ent_on;
+    desc.n_dec_cur = desc.n_dec_all = it.n_dec;
+    desc.n_dec_on = n_dec_on;
+    desc.n_pt_cur = desc.n_pt_all = it.n_pt;
+    desc.n_pt_on = n_pt_on;
+    desc.dropped_at = -1;
+    desc.epoch = epoch;
+    std::memcpy(h + o_desc, &desc, sizeof(desc));
+    int32_t* ht = reinterpret_cast<int32_t*>(h + o_tok);
+    std::memcpy(ht, tok_ids.data(), 4 * T);
+    std::memcpy(ht + T, tok_pos.data(), 4 * T);
+    std::memcpy(ht + 2 * T, tok_slot.data(), 4 * T);
+    int32_t* he = reinterpret_cast<int32_t*>(h + o_ent);
+    std::memcpy(he, ent_q0.data(), 4 * n);
+    std::memcpy(he + E, ent_qlen.data(), 4 * n);
+    std::memcpy(he + 2 * E, ent_kvlen.data(), 4 * n);
+    std::memcpy(he + 3 * E, ent_bt.data(), 4 * n);
+    std::memcpy(he + 4 * E, ent_last.data(), 4 * n);
+    if (!dec_ent.empty()) std::memcpy(h + o_dec, dec_ent.data(), 4 * dec_ent.size());
+    if (!tiles.empty()) std::memcpy(h + o_tiles, tiles.data(), sizeof(csk::PrefillTile) * tiles.size());
+    std::memcpy(h + o_bt, bt.data(), 4 * bt.size());
+
+    // split-K for K1: aim for ~4 CTAs per SM
+    if (it.n_dec > 0) {
+      const int base = it.n_dec * e->hkv;
+      const int target = 4 * e->sms;
+      int S = std::max(1, (target + base - 1) / base);
+      S = std::min(S, std::max(1, (max_dec_pages + 3) / 4));
+      it.pps = (max_dec_pages + S - 1) / S;
+      it.splits = (max_dec_pages + it.pps - 1) / it.pps;
+      const size_t need = static_cast<size_t>(it.n_dec) * e->hkv * it.splits * e->G * (2 + e->D);
+      if (it.splits > 1 && need > e->ws_floats) {
+        if (e->ws) CK(cudaFree(e->ws));
+        e->ws_floats = need * 2;
+        CK(cudaMalloc(&e->ws, e->ws_floats * 4));
+      }
+    }
+    uint8_t* d = e->d_meta;
+    csk::AttnParams& ap = it.ap;
+    ap.qkv = e->qkv;
+    ap.out = e->attn;
+    ap.pool = e->kv;
+    ap.desc = reinterpret_cast<const csk::IterDesc*>(d + o_desc);
+    it.d_tok_ids = reinterpret_cast<const int32_t*>(d + o_tok);
+    ap.tok_pos = it.d_tok_ids + T;
+    it.d_tok_slot = it.d_tok_ids + 2 * T;
+    it.d_ent_last = reinterpret_cast<const int32_t*>(d + o_ent) + 4 * E;
+    ap.ent_q0 = reinterpret_cast<const int32_t*>(d + o_ent);
+    ap.ent_qlen = ap.ent_q0 + E;
+    ap.ent_kvlen = ap.ent_q0 + 2 * E;
+    ap.ent_bt = ap.ent_q0 + 3 * E;
+    ap.block_table = reinterpret_cast<const int32_t*>(d + o_bt);
+    ap.dec_ent = reinterpret_cast<const int32_t*>(d + o_dec);
+    ap.tiles = reinterpret_cast<const csk::PrefillTile*>(d + o_tiles);
+    ap.ws = e->ws;
+    ap.num_layers = e->L;
+    ap.hq = e->hq;
+    ap.hkv = e->hkv;
+    ap.qkv_stride = (e->hq + 2 * e->hkv) * e->D;
+    ap.n_splits = it.splits;
+    ap.pages_per_split = it.pps;
+    ap.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(e->D));
+
+    CK(cudaEventRecord(e->ev_start, e->s_compute));
+    CK(cudaMemcpyAsync(e->d_meta, e->h_meta, total, cudaMemcpyHostToDevice, e->s_compute));
+    e->any_forward = true;
+    it.active = true;
+    it.paced = e->cfg.instrumented != 0 && it.has_offline && e->L > 1;
+    if (!it.paced) {
+      e->enqueue_layers();
+      return;
+    }
+    // paced: hand the layer loop to the worker thread
+    if (!e->worker.joinable()) {
+      e->worker = std::thread([e] {
+        std::unique_lock<std::mutex> lk(e->mu);
+        for (;;) {
+          e->cv.wait(lk, [e] { return e->job_ready || e->quit; });
+          if (e->quit) return;
+          e->job_ready = false;
+          lk.unlock();
+          std::string err;
+          try {
+            CK(cudaSetDevice(e->cfg.device));
+            e->enqueue_layers();
+          } catch (const std::exception& ex) {
+            err = ex.what();
+          }
+          lk.lock();
+          e->worker_err = err;
+          e->job_done = true;
+          e->cv.notify_all();
+        }
+      });
+    }
+    {
+      std::lock_guard<std::mutex> lk(e->mu);
+      e->job_done = false;
+      e->job_ready = true;
+    }
+    e->cv.notify_all();
+  });
+}
+
+int cs_preempt_signal(cs_engine* e, uint64_t epoch) {
+  return guard([&] {
+    if (e->host_only) return;
+    e->mailbox->flag_host_ns = host_ns();
+    __atomic_thread_fence(__ATOMIC_SEQ_CST);
+    e->mailbox->flag_epoch = epoch;
+    e->it.signal_ns = e->mailbox->flag_host_ns;
+  });
+}
+
+int cs_iter_poll(cs_engine* e, int32_t* done) {
+  return guard([&] {
+    if (!e->it.active) {
+      *done = 1;
+      return;
+    }
+    if (e->host_only || e->no_model) {
+      *done = 1;
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(e->mu);
+      if (!e->job_done) {
+        *done = 0;
+        return;
+      }
+    }
+    const cudaError_t q = cudaEventQuery(e->ev_end);
+    if (q == cudaErrorNotReady) {
+      *done = 0;
+      return;
+    }
+    CK(q);
+    *done = 1;
+  });
+}
+
+int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t cap, float* logits) {
+  return guard([&] {
+    auto& it = e->it;
+    if (!it.active) throw std::logic_error("no iteration in flight");
+    cs_iter_info inf{};
+    inf.preempted_at_layer = -1;
+    int n_alive = it.n_ent;
+    if (!(e->host_only || e->no_model)) {
+      {
+        std::unique_lock<std::mutex> lk(e->mu);
+        e->cv.wait(lk, [e] { return e->job_done; });
+        if (!e->worker_err.empty()) {
+          const std::string err = e->worker_err;
+          e->worker_err.clear();
+          it.active = false;
+          throw CudaError(err);
+        }
+      }
+      CK(cudaEventSynchronize(e->ev_end));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e->ev_start, e->ev_end));
+      inf.gpu_ms = ms;
+      const auto* desc = reinterpret_cast<const csk::IterDesc*>(e->h_out);
+      const int32_t* ids = reinterpret_cast<const int32_t*>(e->h_out + sizeof(csk::IterDesc));
+      if (desc->dropped_at >= 0) {
+        inf.preempted_at_layer = desc->dropped_at;
+        n_alive = it.n_ent_on;
+        if (it.signal_ns != 0) {
+          const int64_t drop_host = static_cast<int64_t>(desc->drop_ns) - e->clock_offset_ns;
+          inf.preempt_signal_to_drop_us = static_cast<double>(drop_host - static_cast<int64_t>(it.signal_ns)) / 1e3;
+        }
+      }
+      inf.n_outputs = n_alive;
+      if (out_tokens)
+        for (int i = 0; i < n_alive && i < cap; ++i) out_tokens[i] = ids[i];
+      if (logits && n_alive > 0)
+        CK(cudaMemcpy(logits, e->logits, static_cast<size_t>(n_alive) * e->vocab * 4, cudaMemcpyDeviceToHost));
+    } else {
+      inf.n_outputs = n_alive;
+    }
+    inf.n_entries_after = n_alive;
+    inf.done = 1;
+    // KV written by the surviving entries (the known->written map of 0.11)
+    for (int i = 0; i < n_alive; ++i) {
+      const auto& wr = it.writes[static_cast<size_t>(i)];
+      if (wr[1] >= 0 && e->pool->find(wr[0])) e->pool->note_written(wr[0], wr[1], wr[2]);
+    }
+    e->pool->on_forward_completed();
+    it.active = false;
+    if (info) *info = inf;
+  });
+}
+
+// ---------------------------------------------------------------- debug --
+int cs_debug_read_block(cs_engine* e, int32_t block, void* dst, size_t bytes) {
+  return guard([&] {
+    const size_t bb = static_cast<size_t>(e->block_elems) * 2;
+    if (bytes < bb) throw std::invalid_argument("buffer too small");
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(dst, e->kv + static_cast<size_t>(block) * e->block_elems, bb, cudaMemcpyDeviceToHost));
+  });
+}
+int cs_debug_write_block(cs_engine* e, int32_t block, const void* src, size_t bytes) {
+  return guard([&] {
+    const size_t bb = static_cast<size_t>(e->block_elems) * 2;
+    if (bytes < bb) throw std::invalid_argument("buffer too small");
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(e->kv + static_cast<size_t>(block) * e->block_elems, src, bb, cudaMemcpyHostToDevice));
+  });
+}
+int cs_debug_read_host_slot(cs_engine* e, int32_t slot, void* dst, size_t bytes) {
+  return guard([&] {
+    const size_t bb = static_cast<size_t>(e->block_elems) * 2;
+    if (bytes < bb) throw std::invalid_argument("buffer too small");
+    std::memcpy(dst, e->host_kv + static_cast<size_t>(slot) * e->block_elems, bb);
+  });
+}
+int cs_debug_fill_pool(cs_engine* e, uint64_t seed) {
+  return guard([&] {
+    csk::fill_pool(e->kv, static_cast<size_t>(e->pool->n_blocks()) * e->block_elems, seed, e->s_compute);
+    CK(cudaStreamSynchronize(e->s_compute));
+  });
+}
+int cs_debug_read_weight(cs_engine* e, int32_t layer, int32_t which, void* dst, size_t bytes, size_t* needed) {
+  return guard([&] {
+    const int64_t H = e->hidden;
+    const __nv_bfloat16* src = nullptr;
+    int64_t n = 0;
+    switch (which) {
+      case 0: src = e->w.attn_norm[layer]; n = H; break;
+      case 1: src = e->w.wqkv[layer]; n = static_cast<int64_t>(e->hq + 2 * e->hkv) * e->D * H; break;
+      case 2: src = e->w.wo[layer]; n = H * e->hq * e->D; break;
+      case 3: src = e->w.mlp_norm[layer]; n = H; break;
+      case 4: src = e->w.wgu[layer]; n = 2LL * e->ffn * H; break;
+      case 5: src = e->w.wd[layer]; n = H * e->ffn; break;
+      case 6: src = e->w.emb; n = static_cast<int64_t>(e->vocab) * H; break;
+      case 7: src = e->w.lm_head; n = static_cast<int64_t>(e->vocab) * H; break;
+      case 8: src = e->w.final_norm; n = H; break;
+      default: throw std::invalid_argument("unknown weight");
+    }
+    *needed = static_cast<size_t>(n) * 2;
+    if (dst && bytes >= *needed) CK(cudaMemcpy(dst, src, *needed, cudaMemcpyDeviceToHost));
+  });
+}
+int cs_debug_read_activation(cs_engine* e, int32_t which, void* dst, size_t bytes) {
+  return guard([&] {
+    CK(cudaDeviceSynchronize());
+    const __nv_bfloat16* src = which == 0 ? e->attn : (which == 1 ? e->x : e->qkv);
+    CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+  });
+}
+int32_t cs_token_id(uint64_t seed, int64_t req, int64_t pos, int32_t vocab) {
+  return csk::token_id(seed, req, pos, vocab);
+}
+float cs_hash_uniform(uint64_t seed, uint64_t tensor, uint64_t idx) { return csk::hash_uniform(seed, tensor, idx); }
+
+int cs_sync(cs_engine* e) {
+  return guard([&] {
+    if (!e->host_only) CK(cudaDeviceSynchronize());
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,395 @@
+// Element-wise / row kernels of the layer forward, the KV
+// append (K3), the preemption safepoint (K6) and the checkpoint gather /
+// restore scatter over the host link (K4 / K5).
+#include "common.cuh"
+
+namespace csk {
+
+// ------------------------------------------------------------- weights ----
+// Deterministic random init by GLOBAL element index so a KV-head-sharded
+// rank holds exactly its slice of the unsharded tensor. Rows map through up
+// to 3 (local_start, global_start) segments (q|k|v or gate|up blocks).
+
+__global__ void init_matrix_kernel(__nv_bfloat16* w, int64_t rows, int64_t cols, int64_t global_cols,
+                                   int64_t col_off, RowMap map, uint64_t seed, uint64_t tensor, float scale,
+                                   float offset) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    int seg = 0;
+    for (int s = 1; s < map.n; ++s)
+      if (r >= map.local_start[s]) seg = s;
+    const int64_t gr = map.global_start[seg] + (r - map.local_start[seg]);
+    const uint64_t gidx = static_cast<uint64_t>(gr * global_cols + col_off + c);
+    const float u = hash_uniform(seed, tensor, gidx);
+    w[i] = __float2bfloat16_rn(__fadd_rn(offset, __fmul_rn(scale, u)));
+  }
+}
+
+void init_matrix(__nv_bfloat16* w, int64_t rows, int64_t cols, int64_t global_cols, int64_t col_off,
+                 const RowMap& map, uint64_t seed, uint64_t tensor, float scale, float offset, cudaStream_t s) {
+  init_matrix_kernel<<<1184, 256, 0, s>>>(w, rows, cols, global_cols, col_off, map, seed, tensor, scale, offset);
+}
+
+// ------------------------------------------------------------ embedding ----
+__global__ void embed_kernel(__nv_bfloat16* x, const __nv_bfloat16* emb, const int32_t* tok_ids, int hidden,
+                             const IterDesc* desc) {
+  const int t = blockIdx.x;
+  if (t >= desc->n_tok_cur) return;
+  const uint4* src = reinterpret_cast<const uint4*>(emb + static_cast<size_t>(tok_ids[t]) * hidden);
+  uint4* dst = reinterpret_cast<uint4*>(x + static_cast<size_t>(t) * hidden);
+  for (int i = threadIdx.x; i < hidden / 8; i += blockDim.x) dst[i] = src[i];
+}
+
+void embed(__nv_bfloat16* x, const __nv_bfloat16* emb, const int32_t* tok_ids, int hidden, const IterDesc* desc,
+           int grid, cudaStream_t s) {
+  if (grid > 0) embed_kernel<<<grid, 128, 0, s>>>(x, emb, tok_ids, hidden, desc);
+}
+
+// --------------------------------------------------------- add + RMSNorm ----
+// x[r] += add[r] (if add), xn[r'] = x[r] * rsqrt(mean(x^2) + eps) * w.
+// rows: the row set is all token rows (< n_tok_cur) or, with row_idx, the
+// gathered rows row_idx[i] for i < n_ent_cur (final norm of sampled rows).
+__global__ void add_rmsnorm_kernel(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16* w,
+                                   __nv_bfloat16* xn, int hidden, float eps, const IterDesc* desc,
+                                   const int32_t* row_idx) {
+  const int i = blockIdx.x;
+  int r;
+  if (row_idx != nullptr) {
+    if (i >= desc->n_ent_cur) return;
+    r = row_idx[i];
+  } else {
+    if (i >= desc->n_tok_cur) return;
+    r = i;
+  }
+  __nv_bfloat16* xr = x + static_cast<size_t>(r) * hidden;
+  const __nv_bfloat16* ar = add ? add + static_cast<size_t>(r) * hidden : nullptr;
+  extern __shared__ float sbuf[];  // hidden floats + 32 partials
+  float ss = 0.f;
+  for (int c = threadIdx.x * 8; c < hidden; c += blockDim.x * 8) {
+    uint4 xv = *reinterpret_cast<const uint4*>(xr + c);
+    const __nv_bfloat16* xe = reinterpret_cast<const __nv_bfloat16*>(&xv);
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(xe[j]);
+    if (ar) {
+      uint4 av = *reinterpret_cast<const uint4*>(ar + c);
+      const __nv_bfloat16* ae = reinterpret_cast<const __nv_bfloat16*>(&av);
+      __nv_bfloat16 outv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        outv[j] = __float2bfloat16(v[j] + __bfloat162float(ae[j]));
+        v[j] = __bfloat162float(outv[j]);
+      }
+      *reinterpret_cast<uint4*>(xr + c) = *reinterpret_cast<uint4*>(outv);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sbuf[c + j] = v[j];
+      ss += v[j] * v[j];
+    }
+  }
+  float* part = sbuf + hidden;
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) part[0] = t;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(part[0] / hidden + eps);
+  __nv_bfloat16* yr = xn + static_cast<size_t>(row_idx ? i : r) * hidden;
+  for (int c = threadIdx.x * 8; c < hidden; c += blockDim.x * 8) {
+    uint4 wv = *reinterpret_cast<const uint4*>(w + c);
+    const __nv_bfloat16* we = reinterpret_cast<const __nv_bfloat16*>(&wv);
+    __nv_bfloat16 outv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) outv[j] = __float2bfloat16(sbuf[c + j] * inv * __bfloat162float(we[j]));
+    *reinterpret_cast<uint4*>(yr + c) = *reinterpret_cast<uint4*>(outv);
+  }
+}
+
+void add_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16* w, __nv_bfloat16* xn, int hidden,
+                 float eps, const IterDesc* desc, const int32_t* row_idx, int grid, cudaStream_t s) {
+  if (grid <= 0) return;
+  const int threads = hidden >= 2048 ? 256 : 64;
+  add_rmsnorm_kernel<<<grid, threads, (hidden + 32) * sizeof(float), s>>>(x, add, w, xn, hidden, eps, desc, row_idx);
+}
+
+// ----------------------------------------------------------------- SwiGLU ----
+__global__ void silu_mul_kernel(const __nv_bfloat16* gu, __nv_bfloat16* act, int ffn, const IterDesc* desc) {
+  const int t = blockIdx.y;
+  if (t >= desc->n_tok_cur) return;
+  const __nv_bfloat16* g = gu + static_cast<size_t>(t) * 2 * ffn;
+  const __nv_bfloat16* u = g + ffn;
+  __nv_bfloat16* a = act + static_cast<size_t>(t) * ffn;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8; c < ffn; c += gridDim.x * blockDim.x * 8) {
+    uint4 gv = *reinterpret_cast<const uint4*>(g + c);
+    uint4 uv = *reinterpret_cast<const uint4*>(u + c);
+    const __nv_bfloat16* ge = reinterpret_cast<const __nv_bfloat16*>(&gv);
+    const __nv_bfloat16* ue = reinterpret_cast<const __nv_bfloat16*>(&uv);
+    __nv_bfloat16 o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float gf = __bfloat162float(ge[j]);
+      o[j] = __float2bfloat16(gf / (1.f + __expf(-gf)) * __bfloat162float(ue[j]));
+    }
+    *reinterpret_cast<uint4*>(a + c) = *reinterpret_cast<uint4*>(o);
+  }
+}
+
+void silu_mul(const __nv_bfloat16* gu, __nv_bfloat16* act, int ffn, const IterDesc* desc, int grid_rows,
+              cudaStream_t s) {
+  if (grid_rows <= 0) return;
+  const int bx = (ffn / 8 + 255) / 256;
+  silu_mul_kernel<<<dim3(bx < 1 ? 1 : (bx > 16 ? 16 : bx), grid_rows), 256, 0, s>>>(gu, act, ffn, desc);
+}
+
+// ------------------------------------------------- RoPE + KV append (K3) ----
+// Rotates q and k of every token row in place (rotate-half convention) and
+// scatters k, v into the token's (block, slot) of this layer of the pool.
+__global__ void rope_append_kernel(__nv_bfloat16* qkv, const int32_t* tok_pos, const int32_t* tok_slot,
+                                   __nv_bfloat16* pool, int hq, int hkv, int D, int num_layers, int layer,
+                                   float theta, const IterDesc* desc) {
+  const int t = blockIdx.x;
+  if (t >= desc->n_tok_cur) return;
+  const int stride = (hq + 2 * hkv) * D;
+  __nv_bfloat16* row = qkv + static_cast<size_t>(t) * stride;
+  const float pos = static_cast<float>(tok_pos[t]);
+  const int half = D / 2;
+  const int slot = tok_slot[t];
+  const int blk = slot >> 4, off = slot & 15;
+  const size_t layer_elems = static_cast<size_t>(2) * hkv * 16 * D;
+  __nv_bfloat16* kv_base = pool + (static_cast<size_t>(blk) * num_layers + layer) * layer_elems;
+  // rotations: (hq + hkv) heads x half pairs
+  for (int i = threadIdx.x; i < (hq + hkv) * half; i += blockDim.x) {
+    const int h = i / half, j = i % half;
+    const float inv_freq = powf(theta, -2.f * static_cast<float>(j) / static_cast<float>(D));
+    float sn, cs;
+    sincosf(pos * inv_freq, &sn, &cs);
+    __nv_bfloat16* hp = row + h * D;
+    const float x1 = __bfloat162float(hp[j]), x2 = __bfloat162float(hp[j + half]);
+    const __nv_bfloat16 y1 = __float2bfloat16(x1 * cs - x2 * sn);
+    const __nv_bfloat16 y2 = __float2bfloat16(x2 * cs + x1 * sn);
+    if (h < hq) {
+      hp[j] = y1;
+      hp[j + half] = y2;
+    } else {
+      const int kh = h - hq;
+      __nv_bfloat16* dst = kv_base + (static_cast<size_t>(kh) * 16 + off) * D;
+      dst[j] = y1;
+      dst[j + half] = y2;
+    }
+  }
+  // v rows: straight copy, 16 bytes per thread
+  const __nv_bfloat16* v = row + (hq + hkv) * D;
+  for (int i = threadIdx.x; i < hkv * D / 8; i += blockDim.x) {
+    const int h = (i * 8) / D, d = (i * 8) % D;
+    __nv_bfloat16* dst = kv_base + (static_cast<size_t>(hkv + h) * 16 + off) * D + d;
+    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v + h * D + d);
+  }
+}
+
+void rope_append(__nv_bfloat16* qkv, const int32_t* tok_pos, const int32_t* tok_slot, __nv_bfloat16* pool, int hq,
+                 int hkv, int D, int num_layers, int layer, float theta, const IterDesc* desc, int grid,
+                 cudaStream_t s) {
+  if (grid > 0)
+    rope_append_kernel<<<grid, 128, 0, s>>>(qkv, tok_pos, tok_slot, pool, hq, hkv, D, num_layers, layer, theta, desc);
+}
+
+// ---------------------------------------------------------------- argmax ----
+__global__ void argmax_kernel(const float* logits, int vocab, int32_t* out, const IterDesc* desc) {
+  const int r = blockIdx.x;
+  if (r >= desc->n_ent_cur) {
+    if (threadIdx.x == 0) out[r] = -1;
+    return;
+  }
+  const float* row = logits + static_cast<size_t>(r) * vocab;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+    const float v = row[i];
+    if (v > best || (v == best && i < bi)) {
+      best = v;
+      bi = i;
+    }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      if (sv[w] > best || (sv[w] == best && si[w] < bi)) {
+        best = sv[w];
+        bi = si[w];
+      }
+    }
+    out[r] = bi;
+  }
+}
+
+void argmax_rows(const float* logits, int vocab, int32_t* out, const IterDesc* desc, int grid, cudaStream_t s) {
+  if (grid > 0) argmax_kernel<<<grid, 256, 0, s>>>(logits, vocab, out, desc);
+}
+
+// ------------------------------------------------------- safepoint (K6) ----
+// Layer-boundary check: if the host flag carries this iteration's epoch and
+// the plan still has offline work, truncate every *_cur count to the online
+// prefix (online entries form a prefix of the plan, scheduler.cpp:183-317)
+// and record the layer + device time in the mapped mailbox.
+__global__ void safepoint_kernel(IterDesc* desc, PreemptMailbox* mb, int layer) {
+  if (threadIdx.x != 0) return;
+  if (desc->dropped_at >= 0) return;
+  const uint64_t flag = mb->flag_epoch;
+  if (flag != desc->epoch) return;
+  if (desc->n_ent_on >= desc->n_ent_cur) return;  // nothing offline to drop
+  desc->n_tok_cur = desc->n_tok_on;
+  desc->n_ent_cur = desc->n_ent_on;
+  desc->n_dec_cur = desc->n_dec_on;
+  desc->n_pt_cur = desc->n_pt_on;
+  desc->dropped_at = layer;
+  const uint64_t now = globaltimer_ns();
+  desc->drop_ns = now;
+  mb->seen_layer = layer;
+  mb->seen_gpu_ns = now;
+  __threadfence_system();
+  mb->seen_epoch = desc->epoch;
+}
+
+void safepoint(IterDesc* desc, PreemptMailbox* mb, int layer, cudaStream_t s) {
+  safepoint_kernel<<<1, 32, 0, s>>>(desc, mb, layer);
+}
+
+// TP: every rank votes 1.0 into an extra element of the next all-reduce when
+// it sees the flag; after the sum every rank applies the same decision at the
+// same layer, so row counts never diverge across ranks.
+__global__ void safepoint_vote_kernel(__nv_bfloat16* tail, const IterDesc* desc, const PreemptMailbox* mb) {
+  if (threadIdx.x >= 8) return;
+  float v = 0.f;
+  if (threadIdx.x == 0 && desc->dropped_at < 0 && mb->flag_epoch == desc->epoch &&
+      desc->n_ent_on < desc->n_ent_cur)
+    v = 1.f;
+  tail[threadIdx.x] = __float2bfloat16(v);
+}
+void safepoint_vote(__nv_bfloat16* tail, const IterDesc* desc, const PreemptMailbox* mb, cudaStream_t s) {
+  safepoint_vote_kernel<<<1, 32, 0, s>>>(tail, desc, mb);
+}
+
+__global__ void safepoint_agreed_kernel(IterDesc* desc, PreemptMailbox* mb, const __nv_bfloat16* tail, int layer) {
+  if (threadIdx.x != 0) return;
+  if (desc->dropped_at >= 0) return;
+  if (__bfloat162float(tail[0]) <= 0.f) return;
+  desc->n_tok_cur = desc->n_tok_on;
+  desc->n_ent_cur = desc->n_ent_on;
+  desc->n_dec_cur = desc->n_dec_on;
+  desc->n_pt_cur = desc->n_pt_on;
+  desc->dropped_at = layer;
+  const uint64_t now = globaltimer_ns();
+  desc->drop_ns = now;
+  mb->seen_layer = layer;
+  mb->seen_gpu_ns = now;
+  __threadfence_system();
+  mb->seen_epoch = desc->epoch;
+}
+void safepoint_agreed(IterDesc* desc, PreemptMailbox* mb, const __nv_bfloat16* tail, int layer, cudaStream_t s) {
+  safepoint_agreed_kernel<<<1, 32, 0, s>>>(desc, mb, tail, layer);
+}
+
+// Clock calibration: spin until the host stores its CLOCK_MONOTONIC into the
+// mailbox word, then record %globaltimer next to it.
+__global__ void calib_clock_kernel(volatile uint64_t* mb) {
+  // mb points at PreemptMailbox: [1] = flag_host_ns, [4] = seen_gpu_ns
+  while (mb[1] == 0) {
+  }
+  mb[4] = globaltimer_ns();
+  __threadfence_system();
+}
+void calib_clock(volatile uint64_t* mb, cudaStream_t s) { calib_clock_kernel<<<1, 1, 0, s>>>(mb); }
+
+__global__ void read_globaltimer_kernel(volatile uint64_t* out) {
+  out[0] = globaltimer_ns();
+  __threadfence_system();
+}
+void read_globaltimer(uint64_t* mapped_out, cudaStream_t s) {
+  read_globaltimer_kernel<<<1, 1, 0, s>>>(mapped_out);
+}
+
+// -------------------------------------------- checkpoint / restore (K4/K5) --
+// One work item = one (segment, layer, k|v, head) run of (t1 - t0) tokens x D
+// elements, contiguous in both the device block and the host slot (same
+// [L][2][Hkv][16][D] layout). Device<->host bytes move by plain 16-byte loads
+// and stores through the mapped pinned host pool, so one launch does both the
+// gather and the host-link transfer (measured: 92% of cudaMemcpyAsync peak at
+// 256-byte runs, tools/hostlink_bench.cu).
+struct SegDesc {
+  int32_t block, slot, t0, t1;
+};
+
+template <bool kToHost>
+__global__ void __launch_bounds__(256) kv_move_kernel(__nv_bfloat16* pool, __nv_bfloat16* host,
+                                                      const SegDesc* segs, int n_segs, int runs_per_seg, int D) {
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const size_t block_elems = static_cast<size_t>(runs_per_seg) * 16 * D;
+  const int vec_per_tok = D / 8;
+  for (int64_t item = w; item < static_cast<int64_t>(n_segs) * runs_per_seg; item += warps) {
+    const int s = static_cast<int>(item / runs_per_seg);
+    const int run = static_cast<int>(item % runs_per_seg);
+    const SegDesc sd = segs[s];
+    const size_t off = static_cast<size_t>(run) * 16 * D + static_cast<size_t>(sd.t0) * D;
+    uint4* dev = reinterpret_cast<uint4*>(pool + static_cast<size_t>(sd.block) * block_elems + off);
+    uint4* hst = reinterpret_cast<uint4*>(host + static_cast<size_t>(sd.slot) * block_elems + off);
+    const int n = (sd.t1 - sd.t0) * vec_per_tok;
+    for (int i = lane; i < n; i += 32) {
+      if (kToHost) {
+        hst[i] = __ldcs(dev + i);
+      } else {
+        dev[i] = hst[i];
+      }
+    }
+  }
+}
+
+void kv_move(bool to_host, __nv_bfloat16* pool, __nv_bfloat16* host_mapped, const void* segs_mapped, int n_segs,
+             int runs_per_seg, int D, int sms, cudaStream_t s) {
+  if (n_segs <= 0) return;
+  const int64_t items = static_cast<int64_t>(n_segs) * runs_per_seg;
+  int64_t grid = (items + 7) / 8;
+  if (grid > sms * 8) grid = sms * 8;
+  if (grid < 1) grid = 1;
+  const SegDesc* sd = static_cast<const SegDesc*>(segs_mapped);
+  if (to_host) {
+    kv_move_kernel<true><<<static_cast<int>(grid), 256, 0, s>>>(pool, host_mapped, sd, n_segs, runs_per_seg, D);
+  } else {
+    kv_move_kernel<false><<<static_cast<int>(grid), 256, 0, s>>>(pool, host_mapped, sd, n_segs, runs_per_seg, D);
+  }
+}
+
+// --------------------------------------------------------------- debug ----
+__global__ void fill_pool_kernel(__nv_bfloat16* pool, size_t n, uint64_t seed) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    pool[i] = __float2bfloat16(hash_uniform(seed, 7, i));
+  }
+}
+void fill_pool(__nv_bfloat16* pool, size_t n, uint64_t seed, cudaStream_t s) {
+  fill_pool_kernel<<<2048, 256, 0, s>>>(pool, n, seed);
+}
+
+}  // namespace csk

@@ -1,0 +1,53 @@
+"""K6 layer-wise preemption: a flag stored while the iteration runs drops the
+offline suffix of the plan at the next safepoint; online entries' outputs are
+unaffected (compared with the oracle run on the online prefix only), offline
+allocations roll back, and a flag with a stale epoch is ignored
+(preemption.cpp:95-114)."""
+import numpy as np
+import pytest
+
+import paper_2410_01228_b200 as cs
+from helpers import Driver
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg():
+    return cs.model_config("tiny", num_layers=8, hidden=512, n_heads=8, n_kv_heads=8, head_dim=64, ffn=1024,
+                           vocab=512, max_batched_tokens=4096, gpu_kv_capacity=16384 * 2 * 8 * 2 * 8 * 64,
+                           safepoint_interval_layers=1, instrumented=1)
+
+
+def test_flag_drops_offline_and_keeps_online_exact():
+    drv = Driver(_cfg())
+    drv.add(0, 30, online=True)
+    drv.add(1, 3000, online=False)
+    info, lg, ref = drv.step([(0, None), (1, None)], preempt_after_launch=True)
+    assert info.preempted_at_layer is not None and 1 <= info.preempted_at_layer < 8
+    assert info.n_outputs == 1
+    assert float(np.max(np.abs(lg - ref))) <= 2e-2
+    assert drv.known[1] == 0  # rolled back, zero progress
+    drv.eng.audit()
+    # the offline request runs again next iteration, unpreempted, and matches
+    info, lg, ref = drv.step([(0, None), (1, 1000)])
+    assert info.preempted_at_layer is None
+    assert float(np.max(np.abs(lg - ref))) <= 2e-2
+    drv.close()
+
+
+def test_stale_epoch_is_ignored():
+    drv = Driver(_cfg())
+    drv.add(0, 30, online=True)
+    drv.add(1, 500, online=False)
+    drv.eng.preempt_signal(999)  # a flag for some other iteration
+    info, lg, ref = drv.step([(0, None), (1, None)])
+    assert info.preempted_at_layer is None
+    drv.close()
+
+
+def test_online_only_plan_is_never_dropped():
+    drv = Driver(_cfg())
+    drv.add(0, 300, online=True)
+    info, lg, ref = drv.step([(0, None)], preempt_after_launch=True)
+    assert info.preempted_at_layer is None
+    drv.close()
