@@ -183,6 +183,7 @@ typedef struct {
   int64_t moved_d2h_bytes, moved_h2d_bytes;
   int64_t nonresident_reads;     /* block-table reads of pages the reference marks non-resident (D3) */
   double moved_d2h_ms, moved_h2d_ms;  /* summed device time of the gather / scatter kernels */
+  int64_t kernel_launches;       /* hand-written kernels launched so far (cuBLAS/NCCL excluded) */
 } cs_kv_stats;
 int cs_kv_stats_get(cs_engine* e, cs_kv_stats* out);
 int cs_kv_request_info(cs_engine* e, int64_t id, int64_t* gpu_pages, int64_t* covered_tokens,
@@ -213,7 +214,10 @@ typedef struct {
   int32_t n_entries_after;    /* entries that ran to the end */
   int32_t done;
   double gpu_ms;              /* device time of the iteration (events) */
-  double preempt_signal_to_drop_us; /* host flag store -> device observed (mapped clock) */
+  double preempt_signal_to_drop_us; /* host flag store -> device drop (calibrated clocks) */
+  int64_t h2d_bytes;          /* plan metadata uploaded for this iteration */
+  int64_t d2h_bytes;          /* sampled ids + descriptor read back */
+  int32_t gemm_trunc_layer;   /* first layer whose GEMMs ran on the online rows (-1) */
 } cs_iter_info;
 
 /* Launches the L-layer forward for one plan (online entries must form a
@@ -229,6 +233,30 @@ int cs_preempt_signal(cs_engine* e, uint64_t epoch);
  * written for surviving entries and releases quarantined blocks. */
 int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t cap, float* logits);
 int cs_iter_poll(cs_engine* e, int32_t* done);
+
+/* --------------------------------------------------------------- replay -- */
+/* Replays a recorded reference call log (oracle/lockstep/recorder.cpp) through
+ * this C-ABI: the same sequence of KvCacheManager calls, dispatches,
+ * preemption signals and iteration ends the reference SimEngine issued
+ * (sim_engine.cpp call sites). ops: n_ops records of 8 int64 (see
+ * paper_2410_01228_b200/replay.py for the encoding); plans: 5 int64 per
+ * entry. Iteration outputs (one per DISPATCH in [op_begin, op_end)) go to
+ * the caller's arrays. Returns the number of result mismatches against the
+ * recorded reference results in *mismatches. */
+typedef struct {
+  int64_t iterations, mismatches, first_mismatch_op;
+  double wall_ms;
+} cs_replay_stats;
+int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin, int64_t op_end, const int64_t* plans,
+                  double* gpu_ms, double* wall_end_ms, int32_t* dropped_layer, double* drop_latency_us,
+                  int32_t* gemm_trunc_layer, int64_t* h2d_bytes, int64_t* d2h_bytes, cs_replay_stats* st);
+/* Times the paged-attention kernels (K1/K2) alone for one plan (pages must be
+ * allocated): average ms per launch over reps, algorithmic bytes and flops
+ * per launch. */
+int cs_bench_attention(cs_engine* e, const cs_batch_entry* entries, int32_t n, int32_t reps, double* ms_per_launch,
+                       int64_t* bytes, int64_t* flops);
+/* Dry mode: forwards and transfers are bookkeeping only (fast-forward). */
+int cs_set_dry(cs_engine* e, int32_t dry);
 
 /* ------------------------------------------------------- test / bench hooks -- */
 /* Copies one physical block (all layers of this rank's shard) to host. */

@@ -1,0 +1,111 @@
+"""Generates the golden lockstep call logs from the UNMODIFIED reference
+(oracle/_ref/recorder, built by `make -C oracle recorder`) -- test/bench
+infrastructure only. Output: tests/golden/<scenario>/{run_config.json,
+trace.jsonl, calls.jsonl.gz, metrics.json, requests.jsonl.gz}.
+
+Scenarios:
+  config1  -- tiny CPU co-serving trace: 16 offline (in=96+16i, out=8+i) at
+              t=0 and 4 online (in=64+32i, out=12) at 10/12/40/41 ms; L=2,
+              interval 1, 2048 B/token, 64-page GPU pool, 512-token batches,
+              oracle k1=0.0214 k2=8.36e-7 k4=7e-5 k5=3.5, SLO 50 ms / 20 ms.
+  llama8b  -- Llama-3.1-8B shape (real 131072 B/token, 32 layers), 8192-token
+              batches, a 24 GiB KV pool (so the run evicts, checkpoints and
+              restores), bursty Gamma online trace (rate 3/s, cv 2) 4096/256
+              over 30 s plus a 64-request offline backlog with replenish,
+              8B-preset oracle coefficients (coserve_cli.cpp:45-53), SLO
+              TTFT 0.5 s / TBT 0.1 s, a safepoint every layer.
+"""
+from __future__ import annotations
+
+import gzip
+import json
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+RECORDER = os.path.join(ROOT, "oracle", "_ref", "recorder")
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def _8b_oracle():
+    # calibrate_preset("8b") (coserve_cli.cpp:45-53)
+    chunk, ctx, fresh, deep = 2048.0, 40960.0, 51.0, 124.0
+    k4, k5, k3 = 7e-5, 3.5, 0.0
+    k2 = (deep - fresh - k4 * ctx) / (chunk * ctx)
+    k1 = (fresh - k2 * chunk * chunk - k4 * chunk - k5) / chunk - k3
+    return {"k1": k1, "k2": k2, "k3": k3, "k4": k4, "k5": k5, "noise_cv": 0.0}
+
+
+def scenario(name: str):
+    if name == "config1":
+        trace = [{"t": 0.0, "class": "offline", "in": 96 + 16 * i, "out": 8 + i} for i in range(16)]
+        for i, t in enumerate([0.010, 0.012, 0.040, 0.041]):
+            trace.append({"t": t, "class": "online", "in": 64 + 32 * i, "out": 12})
+        cfg = {
+            "cluster": {"num_layers": 2, "safepoint_interval_layers": 1, "kv_bytes_per_token": 2048,
+                        "gpu_kv_capacity": 64 * 16 * 2048, "host_kv_capacity": 4096 * 16 * 2048,
+                        "d2h_bandwidth": 38797312000.0, "h2d_bandwidth": 38797312000.0,
+                        "safepoint_check_cost_us": 21.0, "gather_cost_us": 500.0, "max_batched_tokens": 512},
+            "oracle": {"k1": 0.0214, "k2": 8.36e-7, "k4": 7e-5, "k5": 3.5},
+            "policy": {"kind": "conserve"},
+            "slo": {"ttft_slo_s": 0.05, "tbt_slo_s": 0.02, "safety_margin": 0.0},
+            "workload": {"trace": "TRACE"},
+            "seed": 1, "audit": True,
+        }
+        return cfg, trace
+    if name == "llama8b":
+        cfg = {
+            "cluster": {"num_layers": 32, "safepoint_interval_layers": 1, "kv_bytes_per_token": 131072,
+                        "gpu_kv_capacity": 24 << 30, "host_kv_capacity": 64 << 30,
+                        "safepoint_check_cost_us": 5.0, "max_batched_tokens": 8192},
+            "oracle": _8b_oracle(),
+            "policy": {"kind": "conserve"},
+            "slo": {"ttft_slo_s": 0.5, "tbt_slo_s": 0.1},
+            "workload": {"online": {"rate": 3.0, "cv": 2.0, "input_tokens": 4096, "output_tokens": 256,
+                                    "duration_s": 30.0},
+                         "offline": {"backlog": 64, "input_tokens": 4096, "output_tokens": 256, "replenish": True}},
+            "seed": 1,
+        }
+        return cfg, None
+    raise SystemExit(f"unknown scenario {name}")
+
+
+def record(name: str) -> str:
+    if not os.path.exists(RECORDER):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "recorder"], check=True)
+    cfg, trace = scenario(name)
+    out = os.path.join(GOLDEN, name)
+    os.makedirs(out, exist_ok=True)
+    with tempfile.TemporaryDirectory() as tmp:
+        if trace is not None:
+            tpath = os.path.join(out, "trace.jsonl")
+            with open(tpath, "w") as f:
+                for t in trace:
+                    f.write(json.dumps(t) + "\n")
+            cfg["workload"]["trace"] = tpath
+        cpath = os.path.join(tmp, "run_config.json")
+        with open(cpath, "w") as f:
+            json.dump(cfg, f, indent=1)
+        r = subprocess.run([RECORDER, cpath, tmp], capture_output=True, text=True)
+        print(r.stdout.strip(), r.stderr.strip())
+        if r.returncode != 0:
+            raise SystemExit(r.returncode)
+        if trace is not None:
+            cfg["workload"]["trace"] = "trace.jsonl"
+        with open(os.path.join(out, "run_config.json"), "w") as f:
+            json.dump(cfg, f, indent=1)
+        for fn in ["calls.jsonl", "requests.jsonl"]:
+            with open(os.path.join(tmp, fn), "rb") as src, gzip.open(os.path.join(out, fn + ".gz"), "wb") as dst:
+                shutil.copyfileobj(src, dst)
+        shutil.copy(os.path.join(tmp, "metrics.json"), os.path.join(out, "metrics.json"))
+        with open(os.path.join(out, "summary.txt"), "w") as f:
+            f.write(r.stdout)
+    return out
+
+
+if __name__ == "__main__":
+    for n in sys.argv[1:] or ["config1", "llama8b"]:
+        print(n, "->", record(n))

@@ -248,16 +248,16 @@ class Oracle:
                 p = rows[i0:i1]
                 kv_len = int(p.max()) + 1
                 K, V = self.kv.read(e.request_id, l, kv_len)
-                qe = q[i0:i1]  # [P, Hq, D]
-                Kg = np.repeat(K, G, axis=1)  # [kv, Hq, D]
-                Vg = np.repeat(V, G, axis=1)
-                sc = np.einsum("phd,khd->hpk", qe, Kg).astype(np.float32) * scale
+                qe = q[i0:i1].reshape(-1, Hkv, G, D)  # [P, Hkv, G, D]; head h = kvh*G + g
+                Kt = np.ascontiguousarray(K.transpose(1, 2, 0))  # [Hkv, D, kv]
+                sc = np.matmul(qe.transpose(1, 2, 0, 3), Kt[:, None]) * scale  # [Hkv, G, P, kv]
                 mask = np.arange(kv_len)[None, :] > p[:, None]
-                sc = np.where(mask[None], -np.inf, sc)
+                sc = np.where(mask[None, None], -np.inf, sc).astype(np.float32)
                 sc = sc - sc.max(axis=-1, keepdims=True)
                 pr = np.exp(sc)
                 pr /= pr.sum(axis=-1, keepdims=True)
-                attn[i0:i1] = np.einsum("hpk,khd->phd", pr, Vg)
+                o = np.matmul(pr, np.ascontiguousarray(V.transpose(1, 0, 2))[:, None])  # [Hkv, G, P, D]
+                attn[i0:i1] = o.transpose(2, 0, 1, 3).reshape(-1, Hq, D)
             attn = self._r(attn.reshape(-1, Hq * D))
             self.last_attn = attn
             o = self._r(attn @ w.wo[l].T)

@@ -84,7 +84,7 @@ class cs_kv_stats(C.Structure):
         ("transfers_inflight", C.c_int32), ("n_blocks", C.c_int64), ("free_blocks", C.c_int64),
         ("quarantined_blocks", C.c_int64), ("n_host_slots", C.c_int64), ("free_host_slots", C.c_int64),
         ("moved_d2h_bytes", C.c_int64), ("moved_h2d_bytes", C.c_int64), ("nonresident_reads", C.c_int64),
-        ("moved_d2h_ms", C.c_double), ("moved_h2d_ms", C.c_double),
+        ("moved_d2h_ms", C.c_double), ("moved_h2d_ms", C.c_double), ("kernel_launches", C.c_int64),
     ]
 
 
@@ -95,7 +95,13 @@ class cs_batch_entry(C.Structure):
 
 class cs_iter_info(C.Structure):
     _fields_ = [("n_outputs", C.c_int32), ("preempted_at_layer", C.c_int32), ("n_entries_after", C.c_int32),
-                ("done", C.c_int32), ("gpu_ms", C.c_double), ("preempt_signal_to_drop_us", C.c_double)]
+                ("done", C.c_int32), ("gpu_ms", C.c_double), ("preempt_signal_to_drop_us", C.c_double),
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("gemm_trunc_layer", C.c_int32)]
+
+
+class cs_replay_stats(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("mismatches", C.c_int64), ("first_mismatch_op", C.c_int64),
+                ("wall_ms", C.c_double)]
 
 
 # (name, argtypes) for every export declared in include/conserve_b200.h
@@ -146,6 +152,12 @@ EXPORTS = {
     "cs_debug_read_activation": ([E, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "cs_debug_read_weight": ([E, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t, P(C.c_size_t)], C.c_int),
     "cs_sync": ([E], C.c_int),
+    "cs_set_dry": ([E, C.c_int32], C.c_int),
+    "cs_bench_attention": ([E, P(cs_batch_entry), C.c_int32, C.c_int32, P(C.c_double), P(C.c_int64),
+                            P(C.c_int64)], C.c_int),
+    "cs_replay_run": ([E, P(C.c_int64), C.c_int64, C.c_int64, P(C.c_int64), P(C.c_double), P(C.c_double),
+                       P(C.c_int32), P(C.c_double), P(C.c_int32), P(C.c_int64), P(C.c_int64),
+                       P(cs_replay_stats)], C.c_int),
     "cs_token_id": ([C.c_uint64, C.c_int64, C.c_int64, C.c_int32], C.c_int32),
     "cs_hash_uniform": ([C.c_uint64, C.c_uint64, C.c_uint64], C.c_float),
 }

@@ -509,10 +509,7 @@ std::optional<cs_transfer_job> BlockPool::flush_checkpoints(int64_t now) {
   job.deltas = std::move(accepted);
   job_ordinal_[info.id] = ++issued_[CS_D2H];
   done_[CS_D2H].push_back(false);
-  if (mover_ != nullptr && !segs.empty()) {
-    mover_->gather_to_host(info.id, segs);
-    job.launched = true;
-  }
+  if (mover_ != nullptr && !segs.empty()) job.launched = mover_->gather_to_host(info.id, segs);
   jobs_.emplace(info.id, std::move(job));
   return info;
 }
@@ -580,10 +577,7 @@ std::optional<cs_transfer_job> BlockPool::start_prefetch(int64_t id, int64_t now
   for (size_t i : targets) job.restores.emplace_back(id, i);
   job_ordinal_[info.id] = ++issued_[CS_H2D];
   done_[CS_H2D].push_back(false);
-  if (mover_ != nullptr) {
-    mover_->scatter_from_host(info.id, segs);
-    job.launched = true;
-  }
+  if (mover_ != nullptr) job.launched = mover_->scatter_from_host(info.id, segs);
   jobs_.emplace(info.id, std::move(job));
   return info;
 }

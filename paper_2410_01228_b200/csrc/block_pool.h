@@ -63,8 +63,9 @@ struct Segment {
 // Data movement backend (engine.cu). Jobs are FIFO per direction.
 struct Mover {
   virtual ~Mover() = default;
-  virtual void gather_to_host(int64_t job_id, const std::vector<Segment>& segs) = 0;
-  virtual void scatter_from_host(int64_t job_id, const std::vector<Segment>& segs) = 0;
+  // Return false when nothing was launched (dry replay): no wait needed.
+  virtual bool gather_to_host(int64_t job_id, const std::vector<Segment>& segs) = 0;
+  virtual bool scatter_from_host(int64_t job_id, const std::vector<Segment>& segs) = 0;
   virtual void wait_job(int64_t job_id) = 0;
   virtual void release_job(int64_t job_id) = 0;
 };

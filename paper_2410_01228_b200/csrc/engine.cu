@@ -171,10 +171,12 @@ struct DeviceMover : csb::Mover {
   };
   std::map<int64_t, Rec> recs;
   explicit DeviceMover(cs_engine* eng) : e(eng) {}
-  void launch(int dir, int64_t job_id, const std::vector<csb::Segment>& segs);
-  void gather_to_host(int64_t job_id, const std::vector<csb::Segment>& segs) override { launch(CS_D2H, job_id, segs); }
-  void scatter_from_host(int64_t job_id, const std::vector<csb::Segment>& segs) override {
-    launch(CS_H2D, job_id, segs);
+  bool launch(int dir, int64_t job_id, const std::vector<csb::Segment>& segs);
+  bool gather_to_host(int64_t job_id, const std::vector<csb::Segment>& segs) override {
+    return launch(CS_D2H, job_id, segs);
+  }
+  bool scatter_from_host(int64_t job_id, const std::vector<csb::Segment>& segs) override {
+    return launch(CS_H2D, job_id, segs);
   }
   void wait_job(int64_t job_id) override;
   void release_job(int64_t job_id) override { recs.erase(job_id); }
@@ -190,6 +192,7 @@ struct Weights {
 struct cs_engine {
   cs_config cfg{};
   bool host_only = false, no_model = false;
+  bool dry = false;  // replay fast-forward: bookkeeping only, no kernels
   int L = 0, hidden = 0, hq = 0, hkv = 0, D = 0, ffn = 0, vocab = 0, G = 0, tp = 1, rank = 0;
   int64_t block_elems = 0;  // per rank, all layers
   int64_t max_tok = 0, max_ent = 0;
@@ -227,6 +230,7 @@ struct cs_engine {
   ncclComm_t comm = nullptr;
   DescRing ring[2];
   double moved_ms[2] = {0, 0};
+  std::atomic<int64_t> launches{0};  // hand-written kernel launches (not cuBLAS/NCCL)
 
   // iteration state
   struct Iter {
@@ -243,6 +247,7 @@ struct cs_engine {
     const int32_t* d_ent_last = nullptr;
     int gemm_trunc_layer = -1;
     uint64_t signal_ns = 0;
+    int64_t meta_bytes = 0;
   } it;
 
   // pacing worker
@@ -260,7 +265,8 @@ struct cs_engine {
 
 namespace {
 
-void DeviceMover::launch(int dir, int64_t job_id, const std::vector<csb::Segment>& segs) {
+bool DeviceMover::launch(int dir, int64_t job_id, const std::vector<csb::Segment>& segs) {
+  if (e->dry) return false;
   Rec r;
   r.ev = std::make_shared<EventPair>();
   r.dir = dir;
@@ -274,9 +280,11 @@ void DeviceMover::launch(int dir, int64_t job_id, const std::vector<csb::Segment
   CK(cudaEventRecord(r.ev->start, st));
   csk::kv_move(dir == CS_D2H, e->kv, e->host_kv_dev, ring.dev + off, static_cast<int>(segs.size()),
                e->L * 2 * e->hkv, e->D, e->sms, st);
+  e->launches += 1;
   CK(cudaGetLastError());
   CK(cudaEventRecord(r.ev->end, st));
   recs.emplace(job_id, std::move(r));
+  return true;
 }
 
 void DeviceMover::wait_job(int64_t job_id) {
@@ -394,6 +402,8 @@ void cs_engine::enqueue_layers() {
         allreduce(tmp, M * hidden);
       }
     }
+    launches += (l == 0 ? 1 : 0) + (is_sp(l) ? 1 : 0) + 4 + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
+                (it.n_dec > 0 ? (it.splits > 1 ? 2 : 1) : 0) + (it.n_pt > 0 ? 1 : 0);
     if (it.paced) CK(cudaEventRecord(ev_layer[l], s_compute));
     if (cfg.flags & CS_FLAG_SYNC_DEBUG) {
       CK(cudaStreamSynchronize(s_compute));
@@ -407,9 +417,195 @@ void cs_engine::enqueue_layers() {
   csk::argmax_rows(logits, vocab, reinterpret_cast<int32_t*>(d_out + sizeof(csk::IterDesc)), desc, E, s_compute);
   CK(cudaMemcpyAsync(d_out, d_meta, sizeof(csk::IterDesc), cudaMemcpyDeviceToDevice, s_compute));
   CK(cudaMemcpyAsync(h_out, d_out, sizeof(csk::IterDesc) + sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s_compute));
+  launches += 2;
   CK(cudaEventRecord(ev_end, s_compute));
   CK(cudaEventRecord(ev_fwd_done, s_compute));
   CK(cudaGetLastError());
+}
+
+// Builds the iteration's device metadata into the pinned
+// staging buffer and the attention parameters; false for bookkeeping-only.
+static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32_t n, uint64_t epoch) {
+    if (e->it.active) throw std::logic_error("iterations overlap on the device");
+    if (n < 1) throw std::invalid_argument("empty batch");
+    if (n > e->max_ent) throw std::invalid_argument("plan has more entries than max_entries");
+    auto& it = e->it;
+    it = cs_engine::Iter{};
+    it.epoch = epoch;
+    it.entries.assign(entries, entries + n);
+    csb::BlockPool& pool = *e->pool;
+
+    // ---- host metadata (SURVEY.md 8a A1): positions per 0.11 ----
+    std::vector<int32_t> tok_ids, tok_pos, tok_slot, ent_q0(n), ent_qlen(n), ent_kvlen(n), ent_bt(n), ent_last(n);
+    std::vector<int32_t> dec_ent, bt;
+    std::vector<csk::PrefillTile> tiles;
+    bool seen_offline = false;
+    int n_tok_on = 0, n_ent_on = 0, n_dec_on = 0, n_pt_on = 0, max_dec_pages = 0;
+    for (int i = 0; i < n; ++i) {
+      const cs_batch_entry& be = entries[i];
+      if (be.online && seen_offline) throw std::invalid_argument("online entries must form a prefix of the plan");
+      if (!be.online) seen_offline = true;
+      const csb::Req* r = pool.find(be.request_id);
+      if (!r) throw std::logic_error("unknown request id in kv manager");
+      std::vector<int32_t> pos;
+      std::array<int64_t, 3> wr{be.request_id, -1, -1};
+      if (be.kind == CS_DECODE) {
+        if (be.compute_tokens != 1 || be.context_tokens < 1) throw std::invalid_argument("decode entry needs P=1, C>=1");
+        pos.push_back(static_cast<int32_t>(be.context_tokens - 1));
+        wr = {be.request_id, be.context_tokens - 1, be.context_tokens};
+      } else if (be.kind == CS_PREFILL) {
+        if (be.compute_tokens < 1) throw std::invalid_argument("prefill entry needs P>=1");
+        for (int64_t p = 0; p < be.compute_tokens; ++p) pos.push_back(static_cast<int32_t>(be.context_tokens + p));
+        wr = {be.request_id, be.context_tokens, be.context_tokens + be.compute_tokens};
+      } else if (be.kind == CS_RECOMPUTE) {
+        // Positions of the pages re-materialized by this build's allocation
+        // (kv_cache.cpp:76-107), page order; BatchEntry.C is context_len.
+        std::vector<size_t> pages;
+        for (const csb::Growth& g : r->growth)
+          if (g.was_discarded) pages.push_back(g.page);
+        std::sort(pages.begin(), pages.end());
+        for (size_t pg : pages)
+          for (int64_t t = 0; t < r->pages[pg].tokens; ++t) pos.push_back(static_cast<int32_t>(pg * 16 + t));
+        if (static_cast<int64_t>(pos.size()) != be.compute_tokens)
+          throw std::logic_error("recompute entry does not match the re-materialized pages");
+      } else {
+        throw std::invalid_argument("unknown entry kind");
+      }
+      const int kv_len = pos.back() + 1;
+      ent_q0[i] = static_cast<int32_t>(tok_pos.size());
+      ent_qlen[i] = static_cast<int32_t>(pos.size());
+      ent_kvlen[i] = kv_len;
+      ent_bt[i] = static_cast<int32_t>(bt.size());
+      const int n_pages = (kv_len + 15) / 16;
+      for (int pg = 0; pg < n_pages; ++pg) bt.push_back(pool.block_for_read(be.request_id, static_cast<size_t>(pg)));
+      for (int32_t p : pos) {
+        tok_ids.push_back(csk::token_id(e->cfg.token_seed, be.request_id, p, e->vocab));
+        tok_pos.push_back(p);
+        tok_slot.push_back(bt[static_cast<size_t>(ent_bt[i] + p / 16)] * 16 + (p % 16));
+      }
+      ent_last[i] = static_cast<int32_t>(tok_pos.size()) - 1;
+      if (pos.size() == 1) {
+        dec_ent.push_back(i);
+        max_dec_pages = std::max(max_dec_pages, n_pages);
+      } else {
+        const int rows = static_cast<int>(pos.size()) * e->G;
+        for (int r0 = 0; r0 < rows; r0 += 64) tiles.push_back({i, r0});
+      }
+      if (be.online) {
+        n_tok_on = static_cast<int>(tok_pos.size());
+        n_ent_on = i + 1;
+        n_dec_on = static_cast<int>(dec_ent.size());
+        n_pt_on = static_cast<int>(tiles.size());
+      }
+      it.writes.push_back(wr);
+    }
+    const int T = static_cast<int>(tok_pos.size());
+    if (T > e->max_tok) throw std::invalid_argument("plan exceeds max_batched_tokens");
+    it.n_tok = T;
+    it.n_tok_on = n_tok_on;
+    it.n_ent = n;
+    it.n_ent_on = n_ent_on;
+    it.n_dec = static_cast<int>(dec_ent.size());
+    it.n_pt = static_cast<int>(tiles.size());
+    it.has_offline = seen_offline;
+    pool.on_forward_launched();
+    if (e->host_only || e->no_model || e->dry) {
+      it.active = true;
+      return false;
+    }
+
+    // ---- pack metadata: [desc | tok_ids | tok_pos | tok_slot | ent x5 (cap max_ent) | dec | tiles | bt] ----
+    const size_t E = static_cast<size_t>(e->max_ent);
+    size_t off = 0;
+    auto region = [&](size_t bytes) {
+      const size_t o = off;
+      off = align_up(off + bytes, 16);
+      return o;
+    };
+    const size_t o_desc = region(sizeof(csk::IterDesc));
+    const size_t o_tok = region(sizeof(int32_t) * 3 * static_cast<size_t>(T));
+    const size_t o_ent = region(sizeof(int32_t) * 5 * E);
+    const size_t o_dec = region(sizeof(int32_t) * dec_ent.size() + 4);
+    const size_t o_tiles = region(sizeof(csk::PrefillTile) * tiles.size() + 8);
+    const size_t o_bt = region(sizeof(int32_t) * bt.size() + 4);
+    const size_t total = off;
+    if (total > e->meta_cap) {
+      if (e->d_meta) CK(cudaFree(e->d_meta));
+      if (e->h_meta) CK(cudaFreeHost(e->h_meta));
+      e->meta_cap = align_up(total * 2, 1 << 20);
+      CK(cudaMalloc(&e->d_meta, e->meta_cap));
+      CK(cudaMallocHost(&e->h_meta, e->meta_cap));
+    }
+    uint8_t* h = e->h_meta;
+    csk::IterDesc desc{};
+    desc.n_tok_cur = desc.n_tok_all = T;
+    desc.n_tok_on = n_tok_on;
+    desc.n_ent_cur = desc.n_ent_all = n;
+    desc.n_ent_on = n_ent_on;
+    desc.n_dec_cur = desc.n_dec_all = it.n_dec;
+    desc.n_dec_on = n_dec_on;
+    desc.n_pt_cur = desc.n_pt_all = it.n_pt;
+    desc.n_pt_on = n_pt_on;
+    desc.dropped_at = -1;
+    desc.epoch = epoch;
+    std::memcpy(h + o_desc, &desc, sizeof(desc));
+    int32_t* ht = reinterpret_cast<int32_t*>(h + o_tok);
+    std::memcpy(ht, tok_ids.data(), 4 * T);
+    std::memcpy(ht + T, tok_pos.data(), 4 * T);
+    std::memcpy(ht + 2 * T, tok_slot.data(), 4 * T);
+    int32_t* he = reinterpret_cast<int32_t*>(h + o_ent);
+    std::memcpy(he, ent_q0.data(), 4 * n);
+    std::memcpy(he + E, ent_qlen.data(), 4 * n);
+    std::memcpy(he + 2 * E, ent_kvlen.data(), 4 * n);
+    std::memcpy(he + 3 * E, ent_bt.data(), 4 * n);
+    std::memcpy(he + 4 * E, ent_last.data(), 4 * n);
+    if (!dec_ent.empty()) std::memcpy(h + o_dec, dec_ent.data(), 4 * dec_ent.size());
+    if (!tiles.empty()) std::memcpy(h + o_tiles, tiles.data(), sizeof(csk::PrefillTile) * tiles.size());
+    std::memcpy(h + o_bt, bt.data(), 4 * bt.size());
+
+    // split-K for K1: aim for ~4 CTAs per SM
+    if (it.n_dec > 0) {
+      const int base = it.n_dec * e->hkv;
+      const int target = 4 * e->sms;
+      int S = std::max(1, (target + base - 1) / base);
+      S = std::min(S, std::max(1, (max_dec_pages + 3) / 4));
+      it.pps = (max_dec_pages + S - 1) / S;
+      it.splits = (max_dec_pages + it.pps - 1) / it.pps;
+      const size_t need = static_cast<size_t>(it.n_dec) * e->hkv * it.splits * e->G * (2 + e->D);
+      if (it.splits > 1 && need > e->ws_floats) {
+        if (e->ws) CK(cudaFree(e->ws));
+        e->ws_floats = need * 2;
+        CK(cudaMalloc(&e->ws, e->ws_floats * 4));
+      }
+    }
+    uint8_t* d = e->d_meta;
+    csk::AttnParams& ap = it.ap;
+    ap.qkv = e->qkv;
+    ap.out = e->attn;
+    ap.pool = e->kv;
+    ap.desc = reinterpret_cast<const csk::IterDesc*>(d + o_desc);
+    it.d_tok_ids = reinterpret_cast<const int32_t*>(d + o_tok);
+    ap.tok_pos = it.d_tok_ids + T;
+    it.d_tok_slot = it.d_tok_ids + 2 * T;
+    it.d_ent_last = reinterpret_cast<const int32_t*>(d + o_ent) + 4 * E;
+    ap.ent_q0 = reinterpret_cast<const int32_t*>(d + o_ent);
+    ap.ent_qlen = ap.ent_q0 + E;
+    ap.ent_kvlen = ap.ent_q0 + 2 * E;
+    ap.ent_bt = ap.ent_q0 + 3 * E;
+    ap.block_table = reinterpret_cast<const int32_t*>(d + o_bt);
+    ap.dec_ent = reinterpret_cast<const int32_t*>(d + o_dec);
+    ap.tiles = reinterpret_cast<const csk::PrefillTile*>(d + o_tiles);
+    ap.ws = e->ws;
+    ap.num_layers = e->L;
+    ap.hq = e->hq;
+    ap.hkv = e->hkv;
+    ap.qkv_stride = (e->hq + 2 * e->hkv) * e->D;
+    ap.n_splits = it.splits;
+    ap.pages_per_split = it.pps;
+    ap.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(e->D));
+    it.meta_bytes = static_cast<int64_t>(total);
+
+    return true;
 }
 
 extern "C" {
@@ -782,6 +978,7 @@ int cs_kv_stats_get(cs_engine* e, cs_kv_stats* o) {
     o->moved_h2d_bytes = p.moved_h2d();
     o->nonresident_reads = p.nonresident_reads();
     o->moved_d2h_ms = e->moved_ms[CS_D2H];
+    o->kernel_launches = e->launches.load();
     o->moved_h2d_ms = e->moved_ms[CS_H2D];
   });
 }
@@ -819,186 +1016,11 @@ int cs_kv_block_table(cs_engine* e, int64_t id, int32_t* blocks, int32_t* slots,
 // ---------------------------------------------------------------- forward --
 int cs_forward_launch(cs_engine* e, const cs_batch_entry* entries, int32_t n, uint64_t epoch) {
   return guard([&] {
-    if (e->it.active) throw std::logic_error("iterations overlap on the device");
-    if (n < 1) throw std::invalid_argument("empty batch");
-    if (n > e->max_ent) throw std::invalid_argument("plan has more entries than max_entries");
+    if (!prepare_iteration(e, entries, n, epoch)) return;
     auto& it = e->it;
-    it = cs_engine::Iter{};
-    it.epoch = epoch;
-    it.entries.assign(entries, entries + n);
-    csb::BlockPool& pool = *e->pool;
-
-    // ---- host metadata (SURVEY.md 8a A1): positions per 0.11 ----
-    std::vector<int32_t> tok_ids, tok_pos, tok_slot, ent_q0(n), ent_qlen(n), ent_kvlen(n), ent_bt(n), ent_last(n);
-    std::vector<int32_t> dec_ent, bt;
-    std::vector<csk::PrefillTile> tiles;
-    bool seen_offline = false;
-    int n_tok_on = 0, n_ent_on = 0, n_dec_on = 0, n_pt_on = 0, max_dec_pages = 0;
-    for (int i = 0; i < n; ++i) {
-      const cs_batch_entry& be = entries[i];
-      if (be.online && seen_offline) throw std::invalid_argument("online entries must form a prefix of the plan");
-      if (!be.online) seen_offline = true;
-      const csb::Req* r = pool.find(be.request_id);
-      if (!r) throw std::logic_error("unknown request id in kv manager");
-      std::vector<int32_t> pos;
-      std::array<int64_t, 3> wr{be.request_id, -1, -1};
-      if (be.kind == CS_DECODE) {
-        if (be.compute_tokens != 1 || be.context_tokens < 1) throw std::invalid_argument("decode entry needs P=1, C>=1");
-        pos.push_back(static_cast<int32_t>(be.context_tokens - 1));
-        wr = {be.request_id, be.context_tokens - 1, be.context_tokens};
-      } else if (be.kind == CS_PREFILL) {
-        if (be.compute_tokens < 1) throw std::invalid_argument("prefill entry needs P>=1");
-        for (int64_t p = 0; p < be.compute_tokens; ++p) pos.push_back(static_cast<int32_t>(be.context_tokens + p));
-        wr = {be.request_id, be.context_tokens, be.context_tokens + be.compute_tokens};
-      } else if (be.kind == CS_RECOMPUTE) {
-        // Positions of the pages re-materialized by this build's allocation
-        // (kv_cache.cpp:76-107), page order; BatchEntry.C is context_len.
-        std::vector<size_t> pages;
-        for (const csb::Growth& g : r->growth)
-          if (g.was_discarded) pages.push_back(g.page);
-        std::sort(pages.begin(), pages.end());
-        for (size_t pg : pages)
-          for (int64_t t = 0; t < r->pages[pg].tokens; ++t) pos.push_back(static_cast<int32_t>(pg * 16 + t));
-        if (static_cast<int64_t>(pos.size()) != be.compute_tokens)
-          throw std::logic_error("recompute entry does not match the re-materialized pages");
-      } else {
-        throw std::invalid_argument("unknown entry kind");
-      }
-      const int kv_len = pos.back() + 1;
-      ent_q0[i] = static_cast<int32_t>(tok_pos.size());
-      ent_qlen[i] = static_cast<int32_t>(pos.size());
-      ent_kvlen[i] = kv_len;
-      ent_bt[i] = static_cast<int32_t>(bt.size());
-      const int n_pages = (kv_len + 15) / 16;
-      for (int pg = 0; pg < n_pages; ++pg) bt.push_back(pool.block_for_read(be.request_id, static_cast<size_t>(pg)));
-      for (int32_t p : pos) {
-        tok_ids.push_back(csk::token_id(e->cfg.token_seed, be.request_id, p, e->vocab));
-        tok_pos.push_back(p);
-        tok_slot.push_back(bt[static_cast<size_t>(ent_bt[i] + p / 16)] * 16 + (p % 16));
-      }
-      ent_last[i] = static_cast<int32_t>(tok_pos.size()) - 1;
-      if (pos.size() == 1) {
-        dec_ent.push_back(i);
-        max_dec_pages = std::max(max_dec_pages, n_pages);
-      } else {
-        const int rows = static_cast<int>(pos.size()) * e->G;
-        for (int r0 = 0; r0 < rows; r0 += 64) tiles.push_back({i, r0});
-      }
-      if (be.online) {
-        n_tok_on = static_cast<int>(tok_pos.size());
-        n_ent_on = i + 1;
-        n_dec_on = static_cast<int>(dec_ent.size());
-        n_pt_on = static_cast<int>(tiles.size());
-      }
-      it.writes.push_back(wr);
-    }
-    const int T = static_cast<int>(tok_pos.size());
-    if (T > e->max_tok) throw std::invalid_argument("plan exceeds max_batched_tokens");
-    it.n_tok = T;
-    it.n_tok_on = n_tok_on;
-    it.n_ent = n;
-    it.n_ent_on = n_ent_on;
-    it.n_dec = static_cast<int>(dec_ent.size());
-    it.n_pt = static_cast<int>(tiles.size());
-    it.has_offline = seen_offline;
-    pool.on_forward_launched();
-    if (e->host_only || e->no_model) {
-      it.active = true;
-      return;
-    }
-
-    // ---- pack metadata: [desc | tok_ids | tok_pos | tok_slot | ent x5 (cap max_ent) | dec | tiles | bt] ----
-    const size_t E = static_cast<size_t>(e->max_ent);
-    size_t off = 0;
-    auto region = [&](size_t bytes) {
-      const size_t o = off;
-      off = align_up(off + bytes, 16);
-      return o;
-    };
-    const size_t o_desc = region(sizeof(csk::IterDesc));
-    const size_t o_tok = region(sizeof(int32_t) * 3 * static_cast<size_t>(T));
-    const size_t o_ent = region(sizeof(int32_t) * 5 * E);
-    const size_t o_dec = region(sizeof(int32_t) * dec_ent.size() + 4);
-    const size_t o_tiles = region(sizeof(csk::PrefillTile) * tiles.size() + 8);
-    const size_t o_bt = region(sizeof(int32_t) * bt.size() + 4);
-    const size_t total = off;
-    if (total > e->meta_cap) {
-      if (e->d_meta) CK(cudaFree(e->d_meta));
-      if (e->h_meta) CK(cudaFreeHost(e->h_meta));
-      e->meta_cap = align_up(total * 2, 1 << 20);
-      CK(cudaMalloc(&e->d_meta, e->meta_cap));
-      CK(cudaMallocHost(&e->h_meta, e->meta_cap));
-    }
-    uint8_t* h = e->h_meta;
-    csk::IterDesc desc{};
-    desc.n_tok_cur = desc.n_tok_all = T;
-    desc.n_tok_on = n_tok_on;
-    desc.n_ent_cur = desc.n_ent_all = n;
-    desc.n_ent_on = n_ent_on;
-    desc.n_dec_cur = desc.n_dec_all = it.n_dec;
-    desc.n_dec_on = n_dec_on;
-    desc.n_pt_cur = desc.n_pt_all = it.n_pt;
-    desc.n_pt_on = n_pt_on;
-    desc.dropped_at = -1;
-    desc.epoch = epoch;
-    std::memcpy(h + o_desc, &desc, sizeof(desc));
-    int32_t* ht = reinterpret_cast<int32_t*>(h + o_tok);
-    std::memcpy(ht, tok_ids.data(), 4 * T);
-    std::memcpy(ht + T, tok_pos.data(), 4 * T);
-    std::memcpy(ht + 2 * T, tok_slot.data(), 4 * T);
-    int32_t* he = reinterpret_cast<int32_t*>(h + o_ent);
-    std::memcpy(he, ent_q0.data(), 4 * n);
-    std::memcpy(he + E, ent_qlen.data(), 4 * n);
-    std::memcpy(he + 2 * E, ent_kvlen.data(), 4 * n);
-    std::memcpy(he + 3 * E, ent_bt.data(), 4 * n);
-    std::memcpy(he + 4 * E, ent_last.data(), 4 * n);
-    if (!dec_ent.empty()) std::memcpy(h + o_dec, dec_ent.data(), 4 * dec_ent.size());
-    if (!tiles.empty()) std::memcpy(h + o_tiles, tiles.data(), sizeof(csk::PrefillTile) * tiles.size());
-    std::memcpy(h + o_bt, bt.data(), 4 * bt.size());
-
-    // split-K for K1: aim for ~4 CTAs per SM
-    if (it.n_dec > 0) {
-      const int base = it.n_dec * e->hkv;
-      const int target = 4 * e->sms;
-      int S = std::max(1, (target + base - 1) / base);
-      S = std::min(S, std::max(1, (max_dec_pages + 3) / 4));
-      it.pps = (max_dec_pages + S - 1) / S;
-      it.splits = (max_dec_pages + it.pps - 1) / it.pps;
-      const size_t need = static_cast<size_t>(it.n_dec) * e->hkv * it.splits * e->G * (2 + e->D);
-      if (it.splits > 1 && need > e->ws_floats) {
-        if (e->ws) CK(cudaFree(e->ws));
-        e->ws_floats = need * 2;
-        CK(cudaMalloc(&e->ws, e->ws_floats * 4));
-      }
-    }
-    uint8_t* d = e->d_meta;
-    csk::AttnParams& ap = it.ap;
-    ap.qkv = e->qkv;
-    ap.out = e->attn;
-    ap.pool = e->kv;
-    ap.desc = reinterpret_cast<const csk::IterDesc*>(d + o_desc);
-    it.d_tok_ids = reinterpret_cast<const int32_t*>(d + o_tok);
-    ap.tok_pos = it.d_tok_ids + T;
-    it.d_tok_slot = it.d_tok_ids + 2 * T;
-    it.d_ent_last = reinterpret_cast<const int32_t*>(d + o_ent) + 4 * E;
-    ap.ent_q0 = reinterpret_cast<const int32_t*>(d + o_ent);
-    ap.ent_qlen = ap.ent_q0 + E;
-    ap.ent_kvlen = ap.ent_q0 + 2 * E;
-    ap.ent_bt = ap.ent_q0 + 3 * E;
-    ap.block_table = reinterpret_cast<const int32_t*>(d + o_bt);
-    ap.dec_ent = reinterpret_cast<const int32_t*>(d + o_dec);
-    ap.tiles = reinterpret_cast<const csk::PrefillTile*>(d + o_tiles);
-    ap.ws = e->ws;
-    ap.num_layers = e->L;
-    ap.hq = e->hq;
-    ap.hkv = e->hkv;
-    ap.qkv_stride = (e->hq + 2 * e->hkv) * e->D;
-    ap.n_splits = it.splits;
-    ap.pages_per_split = it.pps;
-    ap.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(e->D));
-
     CK(cudaEventRecord(e->ev_start, e->s_compute));
-    CK(cudaMemcpyAsync(e->d_meta, e->h_meta, total, cudaMemcpyHostToDevice, e->s_compute));
+    CK(cudaMemcpyAsync(e->d_meta, e->h_meta, static_cast<size_t>(it.meta_bytes), cudaMemcpyHostToDevice,
+                       e->s_compute));
     e->any_forward = true;
     it.active = true;
     it.paced = e->cfg.instrumented != 0 && it.has_offline && e->L > 1;
@@ -1038,6 +1060,47 @@ int cs_forward_launch(cs_engine* e, const cs_batch_entry* entries, int32_t n, ui
   });
 }
 
+// Times the paged-attention kernels alone (layer 0) for one plan: reps
+// back-to-back launches between CUDA events on the compute stream. The plan's
+// pages must be allocated. *bytes = algorithmic K/V + Q/O bytes per launch
+// (sum kv_len*Hkv*d*2*2 + sum P*Hq*d*2*2), *flops = causal
+// attention flops per launch (4*Hq*d per query-key pair).
+int cs_bench_attention(cs_engine* e, const cs_batch_entry* entries, int32_t n, int32_t reps, double* ms_per_launch,
+                       int64_t* bytes, int64_t* flops) {
+  return guard([&] {
+    if (!prepare_iteration(e, entries, n, 0)) throw std::logic_error("attention bench needs a device engine");
+    auto& it = e->it;
+    CK(cudaMemcpyAsync(e->d_meta, e->h_meta, static_cast<size_t>(it.meta_bytes), cudaMemcpyHostToDevice,
+                       e->s_compute));
+    csk::AttnParams ap = it.ap;
+    ap.layer = 0;
+    for (int w = 0; w < 2; ++w) csk::launch_attention(ap, e->D, e->G, it.n_dec, it.n_pt, e->s_compute);
+    CK(cudaEventRecord(e->ev_start, e->s_compute));
+    for (int r = 0; r < reps; ++r) csk::launch_attention(ap, e->D, e->G, it.n_dec, it.n_pt, e->s_compute);
+    CK(cudaEventRecord(e->ev_end, e->s_compute));
+    CK(cudaEventSynchronize(e->ev_end));
+    CK(cudaGetLastError());
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e->ev_start, e->ev_end));
+    *ms_per_launch = ms / reps;
+    int64_t b = 0, f = 0;
+    for (int i = 0; i < n; ++i) {
+      const cs_batch_entry& be = entries[i];
+      const int64_t q = (be.kind == CS_DECODE) ? 1 : be.compute_tokens;
+      const int64_t kv = (be.kind == CS_DECODE) ? be.context_tokens : be.context_tokens + be.compute_tokens;
+      b += kv * e->hkv * e->D * 2 * 2 + q * e->hq * e->D * 2 * 2;
+      // causal pairs: query j (0-based within the chunk) sees C + j + 1 keys
+      const int64_t pairs = (be.kind == CS_DECODE) ? be.context_tokens
+                                                   : q * be.context_tokens + q * (q + 1) / 2;
+      f += pairs * 4LL * e->hq * e->D;
+    }
+    *bytes = b;
+    *flops = f;
+    it.active = false;
+    e->pool->on_forward_completed();
+  });
+}
+
 int cs_preempt_signal(cs_engine* e, uint64_t epoch) {
   return guard([&] {
     if (e->host_only) return;
@@ -1054,7 +1117,7 @@ int cs_iter_poll(cs_engine* e, int32_t* done) {
       *done = 1;
       return;
     }
-    if (e->host_only || e->no_model) {
+    if (e->host_only || e->no_model || e->dry) {
       *done = 1;
       return;
     }
@@ -1081,8 +1144,9 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
     if (!it.active) throw std::logic_error("no iteration in flight");
     cs_iter_info inf{};
     inf.preempted_at_layer = -1;
+    inf.gemm_trunc_layer = -1;
     int n_alive = it.n_ent;
-    if (!(e->host_only || e->no_model)) {
+    if (!(e->host_only || e->no_model || e->dry)) {
       {
         std::unique_lock<std::mutex> lk(e->mu);
         e->cv.wait(lk, [e] { return e->job_done; });
@@ -1108,6 +1172,9 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
         }
       }
       inf.n_outputs = n_alive;
+      inf.h2d_bytes = it.meta_bytes;
+      inf.d2h_bytes = static_cast<int64_t>(sizeof(csk::IterDesc) + sizeof(int32_t) * it.n_ent);
+      inf.gemm_trunc_layer = it.gemm_trunc_layer;
       if (out_tokens)
         for (int i = 0; i < n_alive && i < cap; ++i) out_tokens[i] = ids[i];
       if (logits && n_alive > 0)
@@ -1186,6 +1253,13 @@ int cs_debug_read_activation(cs_engine* e, int32_t which, void* dst, size_t byte
     CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
   });
 }
+int cs_set_dry(cs_engine* e, int32_t dry) {
+  return guard([&] {
+    if (e->it.active) throw std::logic_error("cannot toggle dry mode with an iteration in flight");
+    e->dry = dry != 0;
+  });
+}
+
 int32_t cs_token_id(uint64_t seed, int64_t req, int64_t pos, int32_t vocab) {
   return csk::token_id(seed, req, pos, vocab);
 }
