@@ -70,6 +70,43 @@ def scenario(name: str):
             "seed": 1,
         }
         return cfg, None
+    if name.startswith("config1_"):
+        # the config-1 trace under the other policies / ablations
+        # (policy kinds: config.cpp:38-44; ablation switches: config.hpp:76-82)
+        cfg, trace = scenario("config1")
+        variant = name[len("config1_"):]
+        pol = {"nonpreemptive": {"kind": "non_preemptive"}, "onlineonly": {"kind": "online_only"},
+               "sarathi": {"kind": "sarathi_preemptive"},
+               "noincr": {"kind": "conserve", "incremental_kv": False},
+               "nolayerwise": {"kind": "conserve", "layerwise_preemption": False},
+               "pool48": {"kind": "conserve"}, "pool80": {"kind": "conserve"}}[variant]
+        cfg["policy"] = pol
+        if variant.startswith("pool"):
+            cfg["cluster"]["gpu_kv_capacity"] = int(variant[4:]) * 16 * 2048
+        return cfg, trace
+    if name.startswith("fuzz"):
+        # test_sim_engine.cpp:166-187 ("fuzzed co-serving runs"): base_config
+        # (:14-35) with a 160-page GPU pool at 196608 B/token (= the real
+        # Qwen-2.5-14B shape, 48 layers x 8 KV heads x 128), audit after every
+        # event. Seed 1 is the reference's own crash -> skipped.
+        seed = int(name[4:])
+        pol = {"kind": "conserve"}
+        if seed % 3 == 0:
+            pol = {"kind": "sarathi_preemptive"}
+        if seed % 3 == 1:
+            pol["incremental_kv"] = seed % 2 == 0
+        cfg = {
+            "cluster": {"num_layers": 48, "kv_bytes_per_token": 196608, "gpu_kv_capacity": 196608 * 16 * 160,
+                        "host_kv_capacity": 196608 * 16 * 256},
+            "oracle": {"k1": 0.0214, "k2": 8.36e-7, "k4": 7e-5, "k5": 3.5},
+            "policy": pol,
+            "slo": {"ttft_slo_s": 1.0, "tbt_slo_s": 0.1, "safety_margin": 0.0},
+            "workload": {"online": {"rate": 6.0, "cv": 0.5, "input_tokens": 320, "output_tokens": 24,
+                                    "duration_s": 6.0},
+                         "offline": {"backlog": 6, "input_tokens": 512, "output_tokens": 16}},
+            "seed": seed, "audit": True, "max_sim_time_s": 300.0,
+        }
+        return cfg, None
     raise SystemExit(f"unknown scenario {name}")
 
 
@@ -107,5 +144,8 @@ def record(name: str) -> str:
 
 
 if __name__ == "__main__":
-    for n in sys.argv[1:] or ["config1", "llama8b"]:
+    ALL = ["config1", "llama8b"] + [f"config1_{v}" for v in
+                                    ("nonpreemptive", "onlineonly", "sarathi", "noincr", "nolayerwise", "pool48",
+                                     "pool80")] + [f"fuzz{s}" for s in range(2, 7)]
+    for n in sys.argv[1:] or ALL:
         print(n, "->", record(n))

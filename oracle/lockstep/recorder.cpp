@@ -23,6 +23,7 @@
 //   writes out_dir/calls.jsonl, out_dir/metrics.json, out_dir/requests.jsonl
 #include <cstdio>
 #include <fstream>
+#include <set>
 #include <iostream>
 #include <sstream>
 #include <streambuf>
@@ -40,6 +41,36 @@ using namespace coserve;
 
 static std::FILE* g_out = nullptr;
 static int g_depth = 0;  // nested wrapped calls (none expected; guarded)
+static void emit(const std::string& s);
+static const KvCacheManager* g_kv = nullptr;  // the engine's manager (first wrapped call)
+static std::set<int64_t> g_live;              // registered, not yet released
+
+// FNV-1a over the logical page table of every live request, ascending id:
+// page_table_json (kv_cache.cpp:622-634) | request_gpu_pages | covered_tokens.
+// The replay recomputes the same digest from the B200 engine's block pool
+// (csrc/replay.cpp) -- a per-iteration bit-exact page-table comparison.
+static uint64_t page_table_digest() {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const std::string& s) {
+    for (unsigned char c : s) {
+      h ^= c;
+      h *= 1099511628211ull;
+    }
+  };
+  for (int64_t id : g_live) {
+    mix(g_kv->page_table_json(id));
+    mix("|" + std::to_string(g_kv->request_gpu_pages(id)) + "|" + std::to_string(g_kv->covered_tokens(id)) + "\n");
+  }
+  return h;
+}
+
+static void emit_page_tables(const char* where) {
+  if (!g_kv) return;
+  char buf[160];
+  std::snprintf(buf, sizeof(buf), "{\"op\":\"pt\",\"at\":\"%s\",\"n\":%zu,\"hash\":\"%016llx\"}", where,
+                g_live.size(), static_cast<unsigned long long>(page_table_digest()));
+  emit(buf);
+}
 
 static void emit(const std::string& s) {
   if (g_out) {
@@ -95,6 +126,8 @@ extern "C" {
 void REAL(_ZN7coserve14KvCacheManager16register_requestElb)(KvCacheManager*, int64_t, bool);
 void WRAP(_ZN7coserve14KvCacheManager16register_requestElb)(KvCacheManager* s, int64_t id, bool on) {
   REAL(_ZN7coserve14KvCacheManager16register_requestElb)(s, id, on);
+  g_kv = s;
+  g_live.insert(id);
   emit("{\"op\":\"register\",\"id\":" + std::to_string(id) + ",\"online\":" + (on ? "1" : "0") + "}");
 }
 AllocResult REAL(_ZN7coserve14KvCacheManager8allocateElll)(KvCacheManager*, int64_t, int64_t, int64_t);
@@ -190,12 +223,14 @@ void WRAP(_ZN7coserve14KvCacheManager17on_request_activeEl)(KvCacheManager* s, i
 void REAL(_ZN7coserve14KvCacheManager15release_requestEl)(KvCacheManager*, int64_t);
 void WRAP(_ZN7coserve14KvCacheManager15release_requestEl)(KvCacheManager* s, int64_t id) {
   REAL(_ZN7coserve14KvCacheManager15release_requestEl)(s, id);
+  g_live.erase(id);
   emit("{\"op\":\"release\",\"id\":" + std::to_string(id) + "}");
 }
 
 // ---- forward / safepoint seams ----
 BuildResult REAL(_ZN7coserve9Scheduler11build_batchEl)(Scheduler*, int64_t);
 BuildResult WRAP(_ZN7coserve9Scheduler11build_batchEl)(Scheduler* s, int64_t now) {
+  emit_page_tables("build");
   emit("{\"op\":\"build\",\"now\":" + std::to_string(now) + "}");
   return REAL(_ZN7coserve9Scheduler11build_batchEl)(s, now);
 }
@@ -281,6 +316,16 @@ int main(int argc, char** argv) {
     return 3;
   }
   sink.flush();
+  emit_page_tables("end");
+  // The reference's own invariant audit (kv_cache.cpp:566-620) on the final
+  // state: the replay must reach the same verdict.
+  std::string audit = "ok";
+  try {
+    if (g_kv) g_kv->audit();
+  } catch (const std::exception& e) {
+    audit = e.what();
+  }
+  emit("{\"op\":\"audit\",\"result\":\"" + audit + "\"}");
   std::fclose(g_out);
   std::ofstream(out_dir + "/metrics.json") << rep.to_json_text();
   std::ofstream req(out_dir + "/requests.jsonl");

@@ -6,6 +6,8 @@
 #include <time.h>
 
 #include <cstring>
+#include <set>
+#include <string>
 #include <vector>
 
 #include "../../include/conserve_b200.h"
@@ -14,8 +16,35 @@ namespace {
 enum Op : int64_t {
   kRegister = 0, kAlloc = 1, kCommit = 2, kRollback = 3, kEvict = 4, kDiscard = 5, kReleaseOd = 6, kStage = 7,
   kFlush = 8, kPrefetch = 9, kDone = 10, kPaused = 11, kActive = 12, kRelease = 13, kDispatch = 14, kSignal = 15,
-  kIterEnd = 16, kBuild = 17, kDrop = 18
+  kIterEnd = 16, kBuild = 17, kDrop = 18, kPageTables = 19
 };
+
+// Same digest as oracle/lockstep/recorder.cpp page_table_digest(): FNV-1a over
+// page_table_json | request_gpu_pages | covered_tokens of every live request,
+// ascending id -- computed here from the B200 engine's block pool.
+bool page_table_digest(cs_engine* e, const std::set<int64_t>& live, uint64_t* out) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const char* s, size_t n) {
+    for (size_t i = 0; i < n; ++i) {
+      h ^= static_cast<unsigned char>(s[i]);
+      h *= 1099511628211ull;
+    }
+  };
+  std::string buf(1 << 16, '\0');
+  for (int64_t id : live) {
+    size_t len = 0;
+    if (cs_kv_page_table_json(e, id, nullptr, 0, &len) != CS_OK) return false;
+    if (len + 1 > buf.size()) buf.resize(len + 1);
+    if (cs_kv_page_table_json(e, id, &buf[0], buf.size(), &len) != CS_OK) return false;
+    mix(buf.data(), len);
+    int64_t pages = 0, covered = 0, pending = 0;
+    if (cs_kv_request_info(e, id, &pages, &covered, &pending) != CS_OK) return false;
+    const std::string tail = "|" + std::to_string(pages) + "|" + std::to_string(covered) + "\n";
+    mix(tail.data(), tail.size());
+  }
+  *out = h;
+  return true;
+}
 
 double now_ms() {
   timespec ts;
@@ -36,6 +65,7 @@ extern "C" int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin,
   };
   static uint64_t epoch = 1000;  // distinct from any flag left by earlier runs
   std::vector<cs_batch_entry> entries;
+  std::set<int64_t> live;  // registered, not released (as the recorder tracks them)
   bool inflight = false, signal_armed = false;
   int64_t it = 0;
   const double t0 = now_ms();
@@ -45,6 +75,7 @@ extern "C" int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin,
     switch (o[0]) {
       case kRegister:
         rc = cs_kv_register_request(e, o[1], static_cast<int32_t>(o[2]));
+        live.insert(o[1]);
         break;
       case kAlloc: {
         cs_alloc_result r{};
@@ -104,6 +135,7 @@ extern "C" int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin,
         break;
       case kRelease:
         rc = cs_kv_release_request(e, o[1]);
+        live.erase(o[1]);
         break;
       case kDispatch: {
         const int64_t off = o[1], n = o[2];
@@ -140,6 +172,17 @@ extern "C" int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin,
           if (d2h_bytes) d2h_bytes[it] = info.d2h_bytes;
           ++it;
         }
+        break;
+      }
+      case kPageTables: {
+        // o[1] live requests, o[2] reference digest, o[3] != 0: check enabled
+        if (o[3] == 0) break;
+        uint64_t h = 0;
+        if (!page_table_digest(e, live, &h)) {
+          rc = CS_ERR_LOGIC;
+          break;
+        }
+        if (static_cast<int64_t>(live.size()) != o[1] || static_cast<int64_t>(h) != o[2]) mismatch(i);
         break;
       }
       case kBuild:

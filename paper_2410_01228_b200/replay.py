@@ -23,7 +23,7 @@ from .engine import Engine, _check, lib
 
 OPC = {"register": 0, "allocate": 1, "commit": 2, "rollback": 3, "evict": 4, "discard": 5,
        "release_on_demand": 6, "stage": 7, "flush": 8, "prefetch": 9, "done": 10, "paused": 11, "active": 12,
-       "release": 13, "dispatch": 14, "signal": 15, "iter_end": 16, "build": 17, "drop": 18}
+       "release": 13, "dispatch": 14, "signal": 15, "iter_end": 16, "build": 17, "drop": 18, "pt": 19}
 
 
 @dataclass
@@ -37,6 +37,7 @@ class Trace:
     end_now: np.ndarray          # reference iteration-end time (us)
     dropped: np.ndarray          # reference drop layer per iteration (-1)
     requests: Dict[int, dict] = field(default_factory=dict)
+    audit: Optional[str] = None  # the reference's audit() verdict on its final state
 
     @property
     def n_iter(self) -> int:
@@ -54,6 +55,7 @@ def load(calls_path: str, requests_path: Optional[str] = None) -> Trace:
     plans: List[List[int]] = []
     plan_of, end_plan_of, end_now, dropped = [], [], [], []
     config = {}
+    audit = None
     opener = gzip.open if calls_path.endswith(".gz") else open
     with opener(calls_path, "rt") as f:
         for line in f:
@@ -62,6 +64,9 @@ def load(calls_path: str, requests_path: Optional[str] = None) -> Trace:
                 config = d["config"]
                 continue
             op = d.get("op")
+            if op == "audit":
+                audit = d["result"]
+                continue
             if op is None or op == "completed":
                 continue
             c = OPC[op]
@@ -107,6 +112,9 @@ def load(calls_path: str, requests_path: Optional[str] = None) -> Trace:
                 dropped[-1] = d["layer"]
             elif op == "build":
                 r[1] = d["now"]
+            elif op == "pt":
+                h = int(d["hash"], 16)
+                r[1:4] = [d["n"], h - (1 << 64) if h >= (1 << 63) else h, 1]
             ops.append(r)
     ops_a = np.array(ops, dtype=np.int64).reshape(-1, 8)
     disp = np.nonzero(ops_a[:, 0] == OPC["dispatch"])[0]
@@ -115,7 +123,7 @@ def load(calls_path: str, requests_path: Optional[str] = None) -> Trace:
         ops_a[i, 3] = 1 if dropped[k] >= 0 else 0
     bounds = np.concatenate([[0], disp[1:], [len(ops_a)]]).astype(np.int64)
     tr = Trace(config, ops_a, np.array(plans, dtype=np.int64).reshape(-1, 5), bounds, plan_of, end_plan_of,
-               np.array(end_now, dtype=np.int64), np.array(dropped, dtype=np.int32))
+               np.array(end_now, dtype=np.int64), np.array(dropped, dtype=np.int32), audit=audit)
     if requests_path:
         opener = gzip.open if requests_path.endswith(".gz") else open
         with opener(requests_path, "rt") as f:
@@ -140,8 +148,11 @@ class WindowResult:
     d2h_bytes: np.ndarray
 
 
-def run(eng: Engine, tr: Trace, it_begin: int, it_end: int, dry: bool = False) -> WindowResult:
-    """Executes the ops of iterations [it_begin, it_end) (see bounds)."""
+def run(eng: Engine, tr: Trace, it_begin: int, it_end: int, dry: bool = False,
+        check_page_tables: bool = False) -> WindowResult:
+    """Executes the ops of iterations [it_begin, it_end) (see bounds).
+    check_page_tables compares the logical page table of every live request
+    with the reference's digest at every build (host work: off in benches)."""
     n = it_end - it_begin
     arrs = dict(gpu_ms=np.zeros(n), wall_end_ms=np.zeros(n), dropped_layer=np.full(n, -1, np.int32),
                 drop_latency_us=np.zeros(n), gemm_trunc_layer=np.full(n, -1, np.int32),
@@ -150,7 +161,8 @@ def run(eng: Engine, tr: Trace, it_begin: int, it_end: int, dry: bool = False) -
                                           np.int64: C.c_int64}[v.dtype.type])) for k, v in arrs.items()}
     st = F.cs_replay_stats()
     _check(lib().cs_set_dry(eng._h, 1 if dry else 0))
-    ops = np.ascontiguousarray(tr.ops)
+    ops = np.array(tr.ops)
+    ops[ops[:, 0] == OPC["pt"], 3] = 1 if check_page_tables else 0
     plans = np.ascontiguousarray(tr.plans) if len(tr.plans) else np.zeros((1, 5), np.int64)
     rc = lib().cs_replay_run(eng._h, ops.ctypes.data_as(C.POINTER(C.c_int64)), int(tr.bounds[it_begin]),
                              int(tr.bounds[it_end]), plans.ctypes.data_as(C.POINTER(C.c_int64)),

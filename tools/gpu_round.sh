@@ -1,0 +1,36 @@
+#!/usr/bin/env bash
+# One GPU call: GPU tests, the bench line, the ncu launch list of a short bench
+# run and one `--set full` capture per hot-path kernel. Everything lands in
+# gpurun_out/ (copy the summaries worth keeping into profiles/).
+#   gpurun --timeout 2400 -- 'bash tools/gpu_round.sh [tag] [parts]'
+#   parts: comma list of probe,tests,bench,launches,k1,k2,k4 (default all)
+set -u
+TAG=${1:-r1}
+PARTS=${2:-probe,tests,bench,launches,k1,k2,k4}
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+has() { [[ ",$PARTS," == *",$1,"* ]]; }
+nproc > "$OUT/nproc.txt"
+nvidia-smi -q -d CLOCK > "$OUT/clocks_start.txt" 2>&1
+if has probe; then timeout 300 python tools/probe_box.py > "$OUT/probe.log" 2>&1; cp gpurun_out/probe_box.json "$OUT/" 2>/dev/null; fi
+if has tests; then timeout 900 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_gpu.log"; fi
+if has bench; then timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/bench.err"; fi
+NCU="ncu --clock-control none"
+if has launches; then
+  timeout 900 $NCU --metrics gpu__time_duration.sum -c 6000 --csv --log-file "$OUT/launches.csv" \
+    python bench.py --steps 40 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
+fi
+if has k1; then
+  timeout 600 $NCU --set full --import-source on -k regex:attn_decode_kernel -s 1 -c 1 -o "$OUT/k1_decode" -f \
+    python tools/ncu_targets.py decode > "$OUT/k1.log" 2>&1
+fi
+if has k2; then
+  timeout 600 $NCU --set full --import-source on -k regex:attn_prefill -s 1 -c 1 -o "$OUT/k2_prefill" -f \
+    python tools/ncu_targets.py prefill > "$OUT/k2.log" 2>&1
+fi
+if has k4; then
+  timeout 600 $NCU --set full --import-source on -k regex:kv_move -c 1 -o "$OUT/k4_gather" -f \
+    python tools/ncu_targets.py gather > "$OUT/k4.log" 2>&1
+fi
+nvidia-smi -q -d CLOCK > "$OUT/clocks_end.txt" 2>&1
+echo done

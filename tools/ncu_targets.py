@@ -1,0 +1,74 @@
+"""Short, single-GPU drivers for ncu captures of the hot-path kernels.
+
+  python tools/ncu_targets.py decode    # K1: 64 seqs x 4224 ctx, Llama-3.1-8B heads
+  python tools/ncu_targets.py prefill   # K2: one 2048-token chunk over 4096 cached
+  python tools/ncu_targets.py gather    # K4: checkpoint gather of 1024 whole blocks
+
+Each target launches its kernel a handful of times (ncu replays each launch);
+the numbers printed here are NOT bench values.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2410_01228_b200 as cs  # noqa: E402
+from paper_2410_01228_b200 import _ffi as F  # noqa: E402
+
+
+def _engine(**kw):
+    cfg = cs.model_config("llama8b", hidden=512, ffn=512, vocab=512, gpu_kv_capacity=80 << 30,
+                          host_kv_capacity=4 << 30, max_batched_tokens=8192, instrumented=0, **kw)
+    return cs.Engine(cfg)
+
+
+def bench_attention(eng, plan, reps):
+    arr = (F.cs_batch_entry * len(plan))(*plan)
+    ms, b, f = C.c_double(), C.c_int64(), C.c_int64()
+    cs.engine._check(cs.lib().cs_bench_attention(eng._h, arr, len(plan), reps, C.byref(ms), C.byref(b), C.byref(f)))
+    return ms.value, b.value, f.value
+
+
+def decode(reps=3, n=64, ctx=4224):
+    eng = _engine()
+    plan = []
+    for r in range(n):
+        eng.register_request(r, False)
+        assert eng.allocate(r, ctx + 1).ok
+        eng.commit_allocations(r)
+        plan.append(F.cs_batch_entry(r, 1, ctx, F.CS_DECODE, 0))
+    ms, b, _ = bench_attention(eng, plan, reps)
+    print(f"decode: {ms:.4f} ms/launch, {b} B, {b / ms / 1e6:.1f} GB/s")
+    eng.close()
+
+
+def prefill(reps=3, P=2048, ctx=4096):
+    eng = _engine()
+    eng.register_request(0, False)
+    assert eng.allocate(0, ctx + P).ok
+    eng.commit_allocations(0)
+    ms, _, f = bench_attention(eng, [F.cs_batch_entry(0, P, ctx, F.CS_PREFILL, 0)], reps)
+    print(f"prefill: {ms:.4f} ms/launch, {f} flop, {f / ms / 1e9:.1f} TFLOP/s")
+    eng.close()
+
+
+def gather(n_blocks=1024):
+    eng = _engine()
+    eng.register_request(0, False)
+    assert eng.allocate(0, n_blocks * 16).ok
+    eng.commit_allocations(0)
+    eng.note_written(0, 0, n_blocks * 16)
+    eng.stage_checkpoint(0, 0, n_blocks * 16)
+    job = eng.flush_checkpoints(0)
+    eng.on_transfer_done(job.id, job.done_time)
+    s = eng.stats()
+    print(f"gather: {s.moved_d2h_bytes} B in {s.moved_d2h_ms:.3f} ms = {s.moved_d2h_bytes / s.moved_d2h_ms / 1e6:.1f} GB/s")
+    eng.close()
+
+
+if __name__ == "__main__":
+    {"decode": decode, "prefill": prefill, "gather": gather}[sys.argv[1]]()
