@@ -314,7 +314,11 @@ void validate(const cs_config& c) {
   if (c.head_dim != 64 && c.head_dim != 128) throw ConfigError("head_dim must be 64 or 128");
   if (c.hidden % 8 || (c.ffn / c.tp_size) % 8) throw ConfigError("hidden and ffn shard must be multiples of 8");
   const int64_t model_bpt = 2LL * c.num_layers * c.n_kv_heads * c.head_dim * 2;
-  if (c.kv_bytes_per_token != model_bpt)
+  // Bookkeeping-only engines hold no KV bytes: the reference's accounting
+  // unit may then be any value (its presets use 196608 B/token for every
+  // model, coserve_cli.cpp:56,75,92).
+  if (c.kv_bytes_per_token < 1) throw ConfigError("kv_bytes_per_token must be positive");
+  if (c.kv_bytes_per_token != model_bpt && !(c.flags & CS_FLAG_HOST_ONLY))
     throw ConfigError("kv_bytes_per_token must equal 2*L*H_kv*d*2 = " + std::to_string(model_bpt));
   if (c.gpu_kv_capacity < 1 || c.host_kv_capacity < 1) throw ConfigError("KV capacities must be positive");
   if (c.d2h_bandwidth <= 0 || c.h2d_bandwidth <= 0) throw ConfigError("transfer bandwidths must be positive");

@@ -48,6 +48,6 @@ def test_config_validation_errors():
     cfg = cs.model_config("tiny", flags=cs._ffi.CS_FLAG_HOST_ONLY, page_tokens=32)
     with pytest.raises(cs.CsConfigError, match="page_tokens is fixed at 16"):
         cs.KvPool(cfg)
-    cfg = cs.model_config("tiny", flags=cs._ffi.CS_FLAG_HOST_ONLY, kv_bytes_per_token=196608)
+    cfg = cs.model_config("tiny", flags=0, kv_bytes_per_token=196608)  # validated before any CUDA call
     with pytest.raises(cs.CsConfigError, match="kv_bytes_per_token"):
         cs.KvPool(cfg)
