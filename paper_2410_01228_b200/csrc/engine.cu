@@ -806,11 +806,13 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
           *mbx = t0;
           while (e->mailbox->seen_gpu_ns == 0) {
           }
-          const int64_t off = static_cast<int64_t>(e->mailbox->seen_gpu_ns) - static_cast<int64_t>(t0);
-          if (off < best || rep == 0) best = std::min(best, off);
+          if (e->mailbox->seen_gpu_ns != 1) {  // 1 = the kernel gave up (profiler)
+            const int64_t off = static_cast<int64_t>(e->mailbox->seen_gpu_ns) - static_cast<int64_t>(t0);
+            best = std::min(best, off);
+          }
           CK(cudaStreamSynchronize(e->s_compute));
         }
-        e->clock_offset_ns = best;
+        e->clock_offset_ns = best == INT64_MAX ? 0 : best;
         e->mailbox->flag_host_ns = 0;
         e->mailbox->seen_gpu_ns = 0;
         e->mailbox->seen_epoch = 0;

@@ -313,8 +313,16 @@ void safepoint_agreed(IterDesc* desc, PreemptMailbox* mb, const __nv_bfloat16* t
 // Clock calibration: spin until the host stores its CLOCK_MONOTONIC into the
 // mailbox word, then record %globaltimer next to it.
 __global__ void calib_clock_kernel(volatile uint64_t* mb) {
-  // mb points at PreemptMailbox: [1] = flag_host_ns, [4] = seen_gpu_ns
+  // mb points at PreemptMailbox: [1] = flag_host_ns, [4] = seen_gpu_ns.
+  // Bounded spin: under a profiler that serialises launches the host store
+  // can only come after the kernel exits -- give up after 20 ms (writes 1).
+  const uint64_t t0 = globaltimer_ns();
   while (mb[1] == 0) {
+    if (globaltimer_ns() - t0 > 20000000ull) {
+      mb[4] = 1;
+      __threadfence_system();
+      return;
+    }
   }
   mb[4] = globaltimer_ns();
   __threadfence_system();
