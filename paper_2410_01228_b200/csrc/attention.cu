@@ -8,10 +8,9 @@
 //   XOR-swizzled smem) and keeps its own online softmax; warps and splits are
 //   merged at the end. HBM-bound: the contractions run on mma.sync only to
 //   keep the instruction count far below the byte rate.
-// K2 attn_prefill: multi-query chunks (prefill / recompute) -- FlashAttention-2
-//   style tiles of 64 packed (token, head-in-group) rows x 64 keys with a
-//   causal mask on absolute positions (recompute positions may be
-//   non-contiguous). First version on mma.sync; tcgen05 version: attn_tc.cu.
+// K2 (multi-query chunks: prefill / recompute) runs on tcgen05: attn_tc.cu.
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace csk {
@@ -249,187 +248,15 @@ __global__ void attn_decode_combine_kernel(AttnParams p, int n_dec_grid) {
   }
 }
 
-// ------------------------------------------------------------------- K2 ----
-constexpr int kTileRows = 64;
-constexpr int kTileKeys = 64;
-
-template <int D, int G>
-__global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
-  constexpr int KS = D / 16;
-  constexpr int NTD = D / 8;
-  constexpr int TB = kTileKeys * D * 2;  // bytes per K (or V) tile
-  constexpr int CH = D / 8;
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int tile = blockIdx.x, kvh = blockIdx.y;
-  if (tile >= p.desc->n_pt_cur) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gid = lane >> 2, tig = lane & 3;
-  const PrefillTile t = p.tiles[tile];
-  const int ent = t.entry;
-  const int q0 = p.ent_q0[ent];
-  const int n_rows = p.ent_qlen[ent] * G;
-  const int kv_len = p.ent_kvlen[ent];
-  const int32_t* bt = p.block_table + p.ent_bt[ent];
-  const int n_pages = (kv_len + kPage - 1) / kPage;
-
-  // This thread's two rows.
-  const int ra = t.row0 + warp * 16 + gid, rb = ra + 8;
-  const bool va = ra < n_rows, vb = rb < n_rows;
-  const int last_row = min(t.row0 + kTileRows, n_rows) - 1;
-  const int kv_hi = min(kv_len, p.tok_pos[q0 + last_row / G] + 1);
-  const int pos_a = va ? p.tok_pos[q0 + ra / G] : kv_hi;
-  const int pos_b = vb ? p.tok_pos[q0 + rb / G] : kv_hi;
-
-  uint32_t qa[KS][4];
-  {
-    const __nv_bfloat16* qA = p.qkv + static_cast<size_t>(q0 + (va ? ra : 0) / G) * p.qkv_stride +
-                              static_cast<size_t>(kvh * G + (va ? ra : 0) % G) * D;
-    const __nv_bfloat16* qB = p.qkv + static_cast<size_t>(q0 + (vb ? rb : 0) / G) * p.qkv_stride +
-                              static_cast<size_t>(kvh * G + (vb ? rb : 0) % G) * D;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int d0 = ks * 16 + tig * 2;
-      qa[ks][0] = va ? *reinterpret_cast<const uint32_t*>(qA + d0) : 0u;
-      qa[ks][1] = vb ? *reinterpret_cast<const uint32_t*>(qB + d0) : 0u;
-      qa[ks][2] = va ? *reinterpret_cast<const uint32_t*>(qA + d0 + 8) : 0u;
-      qa[ks][3] = vb ? *reinterpret_cast<const uint32_t*>(qB + d0 + 8) : 0u;
-    }
-  }
-
-  auto load_tile = [&](int kt, int st) {
-    uint8_t* sK = smem + st * 2 * TB;
-    uint8_t* sV = sK + TB;
-#pragma unroll
-    for (int i = 0; i < (kTileKeys * CH) / 128; ++i) {
-      const int c = threadIdx.x + 128 * i;
-      const int r = c / CH, ch = c % CH;
-      const int pgi = kt * (kTileKeys / kPage) + r / kPage;
-      if (pgi < n_pages) {
-        const int32_t blk = bt[pgi];
-        cp_async16(sK + swz<D>(r, ch), kv_page(p, blk, kvh, 0, D) + (r % kPage) * D + ch * 8);
-        cp_async16(sV + swz<D>(r, ch), kv_page(p, blk, kvh, 1, D) + (r % kPage) * D + ch * 8);
-      } else {
-        *reinterpret_cast<uint4*>(sK + swz<D>(r, ch)) = make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(sV + swz<D>(r, ch)) = make_uint4(0, 0, 0, 0);
-      }
-    }
-  };
-
-  float o[NTD][4];
-#pragma unroll
-  for (int i = 0; i < NTD; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-  const int n_kt = (kv_hi + kTileKeys - 1) / kTileKeys;
-  load_tile(0, 0);
-  cp_async_commit();
-  for (int kt = 0; kt < n_kt; ++kt) {
-    const int st = kt & 1;
-    if (kt + 1 < n_kt) load_tile(kt + 1, st ^ 1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const uint8_t* sK = smem + st * 2 * TB;
-    const uint8_t* sV = sK + TB;
-    float s[kTileKeys / 8][4];
-#pragma unroll
-    for (int i = 0; i < kTileKeys / 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-#pragma unroll
-      for (int np = 0; np < kTileKeys / 16; ++np) {
-        const int mi = lane >> 3;
-        const int key = np * 16 + (mi >> 1) * 8 + (lane & 7);
-        uint32_t b0, b1, b2, b3;
-        ldmatrix_x4(b0, b1, b2, b3, sK + swz<D>(key, ks * 2 + (mi & 1)));
-        mma_bf16_16816(s[np * 2], qa[ks], b0, b1);
-        mma_bf16_16816(s[np * 2 + 1], qa[ks], b2, b3);
-      }
-    }
-    const int kbase = kt * kTileKeys;
-    float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-    for (int nt = 0; nt < kTileKeys / 8; ++nt) {
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int key = kbase + nt * 8 + tig * 2 + j;
-        s[nt][j] = (key <= pos_a && key < kv_len) ? s[nt][j] * p.scale_log2 : -INFINITY;
-        s[nt][2 + j] = (key <= pos_b && key < kv_len) ? s[nt][2 + j] * p.scale_log2 : -INFINITY;
-        mx0 = fmaxf(mx0, s[nt][j]);
-        mx1 = fmaxf(mx1, s[nt][2 + j]);
-      }
-    }
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-    const float al0 = mn0 == -INFINITY ? 1.f : exp2f(m0 - mn0);
-    const float al1 = mn1 == -INFINITY ? 1.f : exp2f(m1 - mn1);
-    const float sub0 = mn0 == -INFINITY ? 0.f : mn0;
-    const float sub1 = mn1 == -INFINITY ? 0.f : mn1;
-    m0 = mn0;
-    m1 = mn1;
-    float rs0 = 0.f, rs1 = 0.f;
-    uint32_t pa[kTileKeys / 16][4];
-#pragma unroll
-    for (int nt = 0; nt < kTileKeys / 8; ++nt) {
-      const float p0 = exp2f(s[nt][0] - sub0), p1 = exp2f(s[nt][1] - sub0);
-      const float p2 = exp2f(s[nt][2] - sub1), p3 = exp2f(s[nt][3] - sub1);
-      rs0 += p0 + p1;
-      rs1 += p2 + p3;
-      pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
-      pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
-    }
-    l0 = l0 * al0 + rs0;
-    l1 = l1 * al1 + rs1;
-#pragma unroll
-    for (int i = 0; i < NTD; ++i) {
-      o[i][0] *= al0;
-      o[i][1] *= al0;
-      o[i][2] *= al1;
-      o[i][3] *= al1;
-    }
-#pragma unroll
-    for (int kk = 0; kk < kTileKeys / 16; ++kk) {
-#pragma unroll
-      for (int nd = 0; nd < D / 16; ++nd) {
-        const int mi = lane >> 3;
-        const int key = kk * 16 + (mi & 1) * 8 + (lane & 7);
-        uint32_t v0, v1, v2, v3;
-        ldmatrix_x4_trans(v0, v1, v2, v3, sV + swz<D>(key, nd * 2 + (mi >> 1)));
-        mma_bf16_16816(o[nd * 2], pa[kk], v0, v1);
-        mma_bf16_16816(o[nd * 2 + 1], pa[kk], v2, v3);
-      }
-    }
-    __syncthreads();
-  }
-  cp_async_wait<0>();
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-  const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
-  const size_t ostride = static_cast<size_t>(p.hq) * D;
-#pragma unroll
-  for (int nt = 0; nt < NTD; ++nt) {
-    const int d = nt * 8 + tig * 2;
-    if (va) {
-      __nv_bfloat16* dst = p.out + static_cast<size_t>(q0 + ra / G) * ostride + static_cast<size_t>(kvh * G + ra % G) * D + d;
-      *reinterpret_cast<uint32_t*>(dst) = pack_bf16(o[nt][0] * i0, o[nt][1] * i0);
-    }
-    if (vb) {
-      __nv_bfloat16* dst = p.out + static_cast<size_t>(q0 + rb / G) * ostride + static_cast<size_t>(kvh * G + rb % G) * D + d;
-      *reinterpret_cast<uint32_t*>(dst) = pack_bf16(o[nt][2] * i1, o[nt][3] * i1);
-    }
-  }
-}
-
 // ------------------------------------------------------------- launchers ----
 int decode_smem_bytes(int D) { return 4 * 4 * kPage * D * 2 > (4 * 16 * 2 + 4 * 16 * D) * 4 ? 4 * 4 * kPage * D * 2 : (4 * 16 * 2 + 4 * 16 * D) * 4; }
-int prefill_smem_bytes(int D) { return 2 * 2 * kTileKeys * D * 2; }
+
+bool launch_prefill_tc(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_pt_grid,
+                       cudaStream_t s);
 
 template <int D, int G>
-static void launch_attention_t(const AttnParams& p, int n_dec_grid, int n_pt_grid, cudaStream_t s) {
+static void launch_attention_t(const AttnParams& p, const CUtensorMap* kv_map, int n_dec_grid, int n_pt_grid,
+                               cudaStream_t s) {
   if (n_dec_grid > 0) {
     const int smem = decode_smem_bytes(D);
     static bool attr = false;
@@ -441,22 +268,15 @@ static void launch_attention_t(const AttnParams& p, int n_dec_grid, int n_pt_gri
     attn_decode_kernel<D, G><<<grid, 128, smem, s>>>(p);
     if (p.n_splits > 1) attn_decode_combine_kernel<D, G><<<dim3(n_dec_grid, p.hkv), 128, 0, s>>>(p, n_dec_grid);
   }
-  if (n_pt_grid > 0) {
-    const int smem = prefill_smem_bytes(D);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(attn_prefill_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr = true;
-    }
-    attn_prefill_kernel<D, G><<<dim3(n_pt_grid, p.hkv), 128, smem, s>>>(p);
-  }
+  if (n_pt_grid > 0) launch_prefill_tc(p, kv_map, D, G, n_pt_grid, s);
 }
 
 // Dispatch on (head_dim, group size); returns false for an unsupported shape.
-bool launch_attention(const AttnParams& p, int head_dim, int group, int n_dec_grid, int n_pt_grid, cudaStream_t s) {
+bool launch_attention(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_dec_grid,
+                      int n_pt_grid, cudaStream_t s) {
 #define CS_ATTN_CASE(DD, GG)                                    \
   if (head_dim == DD && group == GG) {                          \
-    launch_attention_t<DD, GG>(p, n_dec_grid, n_pt_grid, s);    \
+    launch_attention_t<DD, GG>(p, kv_map, n_dec_grid, n_pt_grid, s); \
     return true;                                                \
   }
   CS_ATTN_CASE(64, 1)

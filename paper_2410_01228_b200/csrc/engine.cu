@@ -8,6 +8,7 @@
 // GEMM M dimension once a preemption flag is seen, while the device-side
 // safepoint kernel truncates every other kernel at the layer boundary itself.
 #include <cublas_v2.h>
+#include <cuda.h>
 #include <nccl.h>
 #include <time.h>
 
@@ -49,7 +50,8 @@ void calib_clock(volatile uint64_t* mb, cudaStream_t s);
 void kv_move(bool to_host, __nv_bfloat16* pool, __nv_bfloat16* host_mapped, const void* segs_mapped, int n_segs,
              int runs_per_seg, int D, int sms, cudaStream_t s);
 void fill_pool(__nv_bfloat16* pool, size_t n, uint64_t seed, cudaStream_t s);
-bool launch_attention(const AttnParams& p, int head_dim, int group, int n_dec_grid, int n_pt_grid, cudaStream_t s);
+bool launch_attention(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_dec_grid,
+                      int n_pt_grid, cudaStream_t s);
 }  // namespace csk
 
 namespace {
@@ -203,6 +205,7 @@ struct cs_engine {
 
   // device memory
   __nv_bfloat16* kv = nullptr;
+  alignas(64) CUtensorMap kv_map{};  // TMA view of the pool as [rows][D] bf16, 64x16 boxes, 128-B swizzle
   __nv_bfloat16* host_kv = nullptr;      // pinned
   __nv_bfloat16* host_kv_dev = nullptr;  // mapped alias
   void* weight_mem = nullptr;
@@ -325,6 +328,33 @@ void validate(const cs_config& c) {
   if (c.max_batched_tokens < 1) throw ConfigError("max_batched_tokens must be >= 1");
 }
 
+// TMA descriptor for the KV pool viewed as [rows][D] bf16 (a page of one
+// (block, layer, K|V, head) = 16 consecutive rows): 64-column x 16-row boxes,
+// SWIZZLE_128B to match the UMMA operand layout (attn_tc.cu). The driver entry
+// point is resolved through the runtime, so no -lcuda.
+void make_kv_tensor_map(CUtensorMap* map, void* pool, uint64_t rows, int D) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  if (rows >= (1ull << 31)) throw ConfigError("KV pool too large for 32-bit TMA row coordinates");
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), rows};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
+  const cuuint32_t box[2] = {64, 16};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, pool, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ GEMM ----
@@ -389,7 +419,7 @@ void cs_engine::enqueue_layers() {
                      cfg.rope_theta, desc, T, s_compute);
     csk::AttnParams ap = it.ap;
     ap.layer = l;
-    if (!csk::launch_attention(ap, D, G, it.n_dec, it.n_pt, s_compute))
+    if (!csk::launch_attention(ap, &kv_map, D, G, it.n_dec, it.n_pt, s_compute))
       throw ConfigError("unsupported attention shape");
     gemm(attn, w.wo[l], tmp, static_cast<int>(M), hidden, hq * D, false);
     allreduce(tmp, M * hidden);
@@ -492,8 +522,9 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
         dec_ent.push_back(i);
         max_dec_pages = std::max(max_dec_pages, n_pages);
       } else {
+        // K2 tiles: 128 packed (token, head-in-group) rows = the UMMA M
         const int rows = static_cast<int>(pos.size()) * e->G;
-        for (int r0 = 0; r0 < rows; r0 += 64) tiles.push_back({i, r0});
+        for (int r0 = 0; r0 < rows; r0 += 128) tiles.push_back({i, r0});
       }
       if (be.online) {
         n_tok_on = static_cast<int>(tok_pos.size());
@@ -708,6 +739,8 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
 
       const size_t blk_bytes = static_cast<size_t>(e->block_elems) * 2;
       CK(cudaMalloc(&e->kv, static_cast<size_t>(pc.n_blocks) * blk_bytes));
+      CK(cudaMemset(e->kv, 0, static_cast<size_t>(pc.n_blocks) * blk_bytes));  // finite everywhere
+      make_kv_tensor_map(&e->kv_map, e->kv, static_cast<uint64_t>(pc.n_blocks) * e->L * 2 * e->hkv * 16, e->D);
       CK(cudaHostAlloc(&e->host_kv, static_cast<size_t>(pc.n_slots) * blk_bytes,
                        cudaHostAllocMapped | cudaHostAllocPortable));
       CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->host_kv_dev), e->host_kv, 0));
@@ -1080,9 +1113,9 @@ int cs_bench_attention(cs_engine* e, const cs_batch_entry* entries, int32_t n, i
                        e->s_compute));
     csk::AttnParams ap = it.ap;
     ap.layer = 0;
-    for (int w = 0; w < 2; ++w) csk::launch_attention(ap, e->D, e->G, it.n_dec, it.n_pt, e->s_compute);
+    for (int w = 0; w < 2; ++w) csk::launch_attention(ap, &e->kv_map, e->D, e->G, it.n_dec, it.n_pt, e->s_compute);
     CK(cudaEventRecord(e->ev_start, e->s_compute));
-    for (int r = 0; r < reps; ++r) csk::launch_attention(ap, e->D, e->G, it.n_dec, it.n_pt, e->s_compute);
+    for (int r = 0; r < reps; ++r) csk::launch_attention(ap, &e->kv_map, e->D, e->G, it.n_dec, it.n_pt, e->s_compute);
     CK(cudaEventRecord(e->ev_end, e->s_compute));
     CK(cudaEventSynchronize(e->ev_end));
     CK(cudaGetLastError());
