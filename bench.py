@@ -94,6 +94,38 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
+def host_link_peak(device: int):
+    """Pinned cudaMemcpyAsync D2H / H2D GB/s (256 MiB, best of 3) on this box:
+    the denominator of the checkpoint/restore fraction."""
+    import torch
+    n = 256 << 20
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=f"cuda:{device}")
+    s = torch.cuda.Stream(device=device)
+    out = {}
+    for name in ("d2h", "h2d"):
+        best = 1e9
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                e0.record(s)
+                (h.copy_(d, non_blocking=True) if name == "d2h" else d.copy_(h, non_blocking=True))
+                e1.record(s)
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out[name] = n / (best * 1e-3) / 1e9
+    return out
+
+
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the roofline
+    kernel from the committed `ncu --set full` capture (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        return json.load(open(p))
+    return {}
+
+
 def percentile(xs, q):
     """Nearest-rank percentile (reference metrics.cpp:41-48)."""
     if not xs:
@@ -376,6 +408,8 @@ def main():
             cpu.pop("seconds_full_model_equiv", None)
         except Exception as ex:  # the CPU sample must never hide the GPU number
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {ex}"}
+    link_peak = host_link_peak(local)
+    traffic = ncu_traffic()
     host_link = {"d2h_gbs": d2h_b / (d2h_ms * 1e-3) / 1e9 if d2h_ms > 0 else None,
                  "h2d_gbs": h2d_b / (h2d_ms * 1e-3) / 1e9 if h2d_ms > 0 else None,
                  "d2h_bytes": d2h_b, "h2d_bytes": h2d_b}
@@ -396,11 +430,15 @@ def main():
         "slo_tbt_ms": 1e3 * tr.config.get("slo", {}).get("tbt_slo_s", 0.1),
         "offline_tokens": off, "online_tokens": on,
         "preempt": dict(probes.get("preempt", {}), replay_drops=drops),
-        "kv_ckpt": dict(host_link, host_link_peak_gbs={"d2h": 57.2, "h2d": 55.6},
-                        frac_d2h=(host_link["d2h_gbs"] or 0) / 57.2),
+        "kv_ckpt": dict(host_link, host_link_peak_gbs=link_peak,
+                        frac_d2h=(host_link["d2h_gbs"] or 0) / link_peak["d2h"],
+                        frac_h2d=(host_link["h2d_gbs"] or 0) / link_peak["h2d"]),
         "nonresident_reads": nonres,
         "roofline": {"kernel": "attn_decode_kernel<128,4> (K1)", "bound": "hbm", "achieved": dec.get("gbs"),
-                     "peak": hbm_peak, "unit": "GB/s", "frac": dec.get("frac"), "traffic": None,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": dec.get("frac"),
+                     "traffic": traffic.get("K1", {}).get("dram_bytes"),
+                     "algorithmic_bytes": dec.get("bytes"),
+                     "traffic_source": traffic.get("K1", {}).get("source"),
                      "peak_kind": peak_kind,
                      "prefill_K2": probes.get("attention", {}).get("prefill")},
         "cpu_baseline": cpu,

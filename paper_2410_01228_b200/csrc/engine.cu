@@ -52,6 +52,7 @@ void kv_move(bool to_host, __nv_bfloat16* pool, __nv_bfloat16* host_mapped, cons
 void fill_pool(__nv_bfloat16* pool, size_t n, uint64_t seed, cudaStream_t s);
 bool launch_attention(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_dec_grid,
                       int n_pt_grid, cudaStream_t s);
+int prefill_tile_rows();
 }  // namespace csk
 
 namespace {
@@ -522,9 +523,10 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
         dec_ent.push_back(i);
         max_dec_pages = std::max(max_dec_pages, n_pages);
       } else {
-        // K2 tiles: 128 packed (token, head-in-group) rows = the UMMA M
+        // K2 work tiles: prefill_tile_rows() packed (token, head-in-group) rows
         const int rows = static_cast<int>(pos.size()) * e->G;
-        for (int r0 = 0; r0 < rows; r0 += 128) tiles.push_back({i, r0});
+        const int step = csk::prefill_tile_rows();
+        for (int r0 = 0; r0 < rows; r0 += step) tiles.push_back({i, r0});
       }
       if (be.online) {
         n_tok_on = static_cast<int>(tok_pos.size());

@@ -1,0 +1,130 @@
+"""Kernel-level parity of K1 (decode) and K2 (tcgen05 prefill) paged
+attention at Llama-3.1-8B head shapes (32 q heads, 8 KV heads, d=128),
+against an fp32 numpy reference computed from the device's own bf16 inputs:
+q from the post-RoPE qkv activation, K/V read back from the HBM blocks the
+block table names. Covers multi-tile causal chunks over a cached context,
+partial pages, GQA grouping, several entries in one launch and the lazy
+O-rescale path (a late, large score). Tolerance: rel-L2 <= 1e-2 per row
+block (bf16 P/V products, fp32 accumulation)."""
+import numpy as np
+import pytest
+
+import paper_2410_01228_b200 as cs
+from oracle import numeric as N
+
+pytestmark = pytest.mark.gpu
+
+HQ, HKV, D = 32, 8, 128
+G = HQ // HKV
+
+
+def _engine():
+    cfg = cs.model_config("tiny", num_layers=1, hidden=512, n_heads=HQ, n_kv_heads=HKV, head_dim=D, ffn=512,
+                          vocab=512, max_batched_tokens=4096, gpu_kv_capacity=(1 << 14) * 16 * 2 * HKV * D * 2,
+                          rope_theta=500000.0, instrumented=0)
+    return cs.Engine(cfg)
+
+
+def _kv_of(eng, rid, n_pos):
+    blocks, _ = eng.block_table(rid)
+    K = np.zeros((n_pos, HKV, D), np.float32)
+    V = np.zeros((n_pos, HKV, D), np.float32)
+    for pg in range((n_pos + 15) // 16):
+        blk = N.from_bf16_bits(eng.read_block(blocks[pg])).reshape(1, 2, HKV, 16, D)[0]
+        n = min(16, n_pos - pg * 16)
+        K[pg * 16:pg * 16 + n] = blk[0, :, :n].transpose(1, 0, 2)
+        V[pg * 16:pg * 16 + n] = blk[1, :, :n].transpose(1, 0, 2)
+    return K, V
+
+
+def _ref_rows(q, K, V, positions):
+    """q [T, HQ, D] fp32; K/V [n, HKV, D]; row t attends keys [0, positions[t]]."""
+    out = np.zeros_like(q)
+    scale = 1.0 / np.sqrt(D)
+    for t, pos in enumerate(positions):
+        for h in range(HQ):
+            s = K[:pos + 1, h // G] @ q[t, h] * scale
+            s = np.exp(s - s.max())
+            out[t, h] = (s / s.sum()) @ V[:pos + 1, h // G]
+    return out
+
+
+def _run(eng, entries, allocs):
+    for e, n in zip(entries, allocs):
+        assert eng.allocate(e.request_id, n).ok
+    eng.forward_launch(entries, 1)
+    eng.iter_wait()
+    for e in entries:
+        eng.commit_allocations(e.request_id)
+
+
+def _check_rows(eng, entries, row_pos, T):
+    qkv = N.from_bf16_bits(eng.read_activation(2, T, (HQ + 2 * HKV) * D))
+    got = N.from_bf16_bits(eng.read_activation(0, T, HQ * D)).reshape(T, HQ, D)
+    row = 0
+    for e, positions in zip(entries, row_pos):
+        n = len(positions)
+        K, V = _kv_of(eng, e.request_id, max(positions) + 1)
+        q = qkv[row:row + n, :HQ * D].reshape(n, HQ, D)
+        want = _ref_rows(q, K, V, positions)
+        err = np.linalg.norm(got[row:row + n] - want) / np.linalg.norm(want)
+        assert err <= 1e-2, (e, err)
+        row += n
+
+
+def test_k2_prefill_chunks_over_cached_context():
+    eng = _engine()
+    try:
+        eng.register_request(0, False)
+        eng.register_request(1, True)
+        # chunk 1: 700 fresh tokens of request 0 (single-tile and multi-tile CTAs)
+        e0 = cs.BatchEntry(0, 700, 0, cs.CS_PREFILL, False)
+        _run(eng, [e0], [700])
+        # chunk 2 of request 0 (C=700, P=1100: crosses 128-key tiles and partial
+        # pages) next to a fresh 333-token online prefill
+        e1 = cs.BatchEntry(1, 333, 0, cs.CS_PREFILL, True)
+        e2 = cs.BatchEntry(0, 1100, 700, cs.CS_PREFILL, False)
+        _run(eng, [e1, e2], [334, 1101])
+        _check_rows(eng, [e1, e2], [list(range(333)), list(range(700, 1800))], 333 + 1100)
+    finally:
+        eng.close()
+
+
+def test_k1_decode_and_k2_in_one_launch():
+    eng = _engine()
+    try:
+        for r in range(5):
+            eng.register_request(r, r == 0)
+        ctx = [1, 17, 300, 2049, 4000]
+        for r, c in enumerate(ctx):  # write context KV with a prefill of c tokens
+            _run(eng, [cs.BatchEntry(r, c, 0, cs.CS_PREFILL, r == 0)], [c + 1])
+        dec = [cs.BatchEntry(r, 1, c + 1, cs.CS_DECODE, r == 0) for r, c in enumerate(ctx)]
+        eng.register_request(9, False)
+        pre = cs.BatchEntry(9, 257, 0, cs.CS_PREFILL, False)
+        _run(eng, dec + [pre], [1] * 5 + [257])
+        _check_rows(eng, dec + [pre], [[c] for c in ctx] + [list(range(257))], 5 + 257)
+    finally:
+        eng.close()
+
+
+def test_k2_lazy_rescale_path():
+    """A key late in the sequence with a much larger score than everything
+    before forces the O-in-TMEM correction (max grows by > 2^8 in log2 units)."""
+    eng = _engine()
+    try:
+        eng.register_request(0, False)
+        _run(eng, [cs.BatchEntry(0, 600, 0, cs.CS_PREFILL, False)], [600])
+        # blow up K at position 500 for every head: huge positive dot with q
+        blocks, _ = eng.block_table(0)
+        blk = N.from_bf16_bits(eng.read_block(blocks[500 // 16])).reshape(2, HKV, 16, D)
+        qkv = N.from_bf16_bits(eng.read_activation(2, 600, (HQ + 2 * HKV) * D))
+        for h in range(HKV):
+            qv = qkv[550, h * G * D:(h * G + 1) * D]
+            blk[0, h, 500 % 16] = 40.0 * np.sign(qv)
+        eng.write_block(blocks[500 // 16], N.bf16_bits(blk.reshape(-1)))
+        # a second chunk attends over the modified cache
+        e = cs.BatchEntry(0, 300, 600, cs.CS_PREFILL, False)
+        _run(eng, [e], [300])
+        _check_rows(eng, [e], [list(range(600, 900))], 300)
+    finally:
+        eng.close()
