@@ -70,6 +70,16 @@ def scenario(name: str):
             "seed": 1,
         }
         return cfg, None
+    if name == "llama8b_b200":
+        # the llama8b scenario with the reference scheduler planning on
+        # B200-measured latencies: oracle coefficients = the reference's own
+        # fit (oracle/_ref/fit_profile) of the engine profiled on a B200 over
+        # default_profile_grid (tools/profile_b200.py -> profiles/b200_fit.json)
+        cfg, _ = scenario("llama8b")
+        fit = json.load(open(os.path.join(ROOT, "profiles", "b200_fit.json")))["coeffs"]
+        cfg["oracle"] = {"k1": fit["a_lin"], "k2": fit["a_quad"], "k3": 0.0, "k4": fit["a_mem"],
+                         "k5": fit["a_const"], "noise_cv": 0.0}
+        return cfg, None
     if name.startswith("config1_"):
         # the config-1 trace under the other policies / ablations
         # (policy kinds: config.cpp:38-44; ablation switches: config.hpp:76-82)

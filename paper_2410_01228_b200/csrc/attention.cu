@@ -218,9 +218,14 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
   }
 }
 
-// Split-K merge for K1: one CTA per (entry, KV head), thread per (row, dim).
+// Split-K merge for K1: one CTA per (entry, KV head). The per-split (max,
+// sum) pairs are staged once in shared memory with the merge weights, then
+// every thread sums its (row, dim) over the splits with independent loads.
 template <int D, int G>
-__global__ void attn_decode_combine_kernel(AttnParams p, int n_dec_grid) {
+__global__ void __launch_bounds__(256) attn_decode_combine_kernel(AttnParams p, int n_dec_grid) {
+  constexpr int kMaxSplits = 128;
+  __shared__ float wgt[kMaxSplits * G];  // exp2(m_s - M) per (split, row)
+  __shared__ float inv_l[G];
   const int kvh = blockIdx.y, di = blockIdx.x;
   if (di >= p.desc->n_dec_cur) return;
   const int S = p.n_splits;
@@ -229,22 +234,31 @@ __global__ void attn_decode_combine_kernel(AttnParams p, int n_dec_grid) {
   const size_t base_item = (static_cast<size_t>(di) * p.hkv + kvh) * S;
   const float* wm = p.ws + base_item * G * 2;
   const float* wo = p.ws + static_cast<size_t>(n_dec_grid) * p.hkv * S * G * 2 + base_item * G * D;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < G; r += blockDim.x >> 5) {
+    float M = -INFINITY;
+    for (int s = lane; s < S; s += 32) M = fmaxf(M, wm[(s * G + r) * 2]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float L = 0.f;
+    for (int s = lane; s < S; s += 32) {
+      const float ms = wm[(s * G + r) * 2];
+      const float f = (M == -INFINITY || ms == -INFINITY) ? 0.f : exp2f(ms - M);
+      wgt[s * G + r] = f;
+      L += wm[(s * G + r) * 2 + 1] * f;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (lane == 0) inv_l[r] = L > 0.f ? 1.f / L : 0.f;
+  }
+  __syncthreads();
   for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
     const int r = idx / D, d = idx % D;
-    float M = -INFINITY;
-    for (int s = 0; s < S; ++s) M = fmaxf(M, wm[(s * G + r) * 2]);
-    float L = 0.f, O = 0.f;
-    if (M != -INFINITY) {
-      for (int s = 0; s < S; ++s) {
-        const float ms = wm[(s * G + r) * 2];
-        if (ms == -INFINITY) continue;
-        const float f = exp2f(ms - M);
-        L += wm[(s * G + r) * 2 + 1] * f;
-        O += wo[(s * G + r) * D + d] * f;
-      }
-    }
+    float O = 0.f;
+#pragma unroll 8
+    for (int s = 0; s < S; ++s) O += wo[(s * G + r) * D + d] * wgt[s * G + r];
     p.out[static_cast<size_t>(row) * p.hq * D + static_cast<size_t>(kvh * G + r) * D + d] =
-        __float2bfloat16(L > 0.f ? O / L : 0.f);
+        __float2bfloat16(O * inv_l[r]);
   }
 }
 
@@ -266,7 +280,7 @@ static void launch_attention_t(const AttnParams& p, const CUtensorMap* kv_map, i
     }
     dim3 grid(p.n_splits, p.hkv, n_dec_grid);
     attn_decode_kernel<D, G><<<grid, 128, smem, s>>>(p);
-    if (p.n_splits > 1) attn_decode_combine_kernel<D, G><<<dim3(n_dec_grid, p.hkv), 128, 0, s>>>(p, n_dec_grid);
+    if (p.n_splits > 1) attn_decode_combine_kernel<D, G><<<dim3(n_dec_grid, p.hkv), 256, 0, s>>>(p, n_dec_grid);
   }
   if (n_pt_grid > 0) launch_prefill_tc(p, kv_map, D, G, n_pt_grid, s);
 }

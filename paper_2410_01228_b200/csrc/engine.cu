@@ -16,6 +16,7 @@
 #include <array>
 #include <atomic>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -606,6 +607,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
       const int target = 4 * e->sms;
       int S = std::max(1, (target + base - 1) / base);
       S = std::min(S, std::max(1, (max_dec_pages + 3) / 4));
+      S = std::min(S, 128);  // attn_decode_combine_kernel stages <= 128 splits
       it.pps = (max_dec_pages + S - 1) / S;
       it.splits = (max_dec_pages + it.pps - 1) / it.pps;
       const size_t need = static_cast<size_t>(it.n_dec) * e->hkv * it.splits * e->G * (2 + e->D);
@@ -1064,7 +1066,14 @@ int cs_forward_launch(cs_engine* e, const cs_batch_entry* entries, int32_t n, ui
                        e->s_compute));
     e->any_forward = true;
     it.active = true;
-    it.paced = e->cfg.instrumented != 0 && it.has_offline && e->L > 1;
+    // CS_NO_PACING=1 (profilers that serialise launches across threads):
+    // enqueue every layer from the caller; the device safepoint still drops
+    // offline work, only the host-side GEMM shrink is lost.
+    static const bool no_pacing = [] {
+      const char* v = std::getenv("CS_NO_PACING");
+      return v && v[0] == '1';
+    }();
+    it.paced = e->cfg.instrumented != 0 && it.has_offline && e->L > 1 && !no_pacing;
     if (!it.paced) {
       e->enqueue_layers();
       return;

@@ -151,38 +151,43 @@ void silu_mul(const __nv_bfloat16* gu, __nv_bfloat16* act, int ffn, const IterDe
 // ------------------------------------------------- RoPE + KV append (K3) ----
 // Rotates q and k of every token row in place (rotate-half convention) and
 // scatters k, v into the token's (block, slot) of this layer of the pool.
-__global__ void rope_append_kernel(__nv_bfloat16* qkv, const int32_t* tok_pos, const int32_t* tok_slot,
-                                   __nv_bfloat16* pool, int hq, int hkv, int D, int num_layers, int layer,
-                                   float theta, const IterDesc* desc) {
+// One CTA per token: the D/2 (cos, sin) pairs of the token's position are
+// computed once (accurate sincosf: positions reach 64K) and shared by all
+// Hq + Hkv heads; rotations move bf16x2 pairs, v moves 16-B vectors.
+__global__ void __launch_bounds__(256) rope_append_kernel(__nv_bfloat16* qkv, const int32_t* tok_pos,
+                                                          const int32_t* tok_slot, __nv_bfloat16* pool, int hq,
+                                                          int hkv, int D, int num_layers, int layer, float theta,
+                                                          const IterDesc* desc) {
   const int t = blockIdx.x;
   if (t >= desc->n_tok_cur) return;
+  __shared__ float2 rot[128];  // (cos, sin) per frequency, D <= 256
   const int stride = (hq + 2 * hkv) * D;
   __nv_bfloat16* row = qkv + static_cast<size_t>(t) * stride;
   const float pos = static_cast<float>(tok_pos[t]);
   const int half = D / 2;
+  for (int j = threadIdx.x; j < half; j += blockDim.x) {
+    const float inv_freq = powf(theta, -2.f * static_cast<float>(j) / static_cast<float>(D));
+    float sn, cs;
+    sincosf(pos * inv_freq, &sn, &cs);
+    rot[j] = make_float2(cs, sn);
+  }
+  __syncthreads();
   const int slot = tok_slot[t];
   const int blk = slot >> 4, off = slot & 15;
   const size_t layer_elems = static_cast<size_t>(2) * hkv * 16 * D;
   __nv_bfloat16* kv_base = pool + (static_cast<size_t>(blk) * num_layers + layer) * layer_elems;
-  // rotations: (hq + hkv) heads x half pairs
-  for (int i = threadIdx.x; i < (hq + hkv) * half; i += blockDim.x) {
-    const int h = i / half, j = i % half;
-    const float inv_freq = powf(theta, -2.f * static_cast<float>(j) / static_cast<float>(D));
-    float sn, cs;
-    sincosf(pos * inv_freq, &sn, &cs);
+  const int pairs = half / 2;  // bf16x2 pairs per half-row
+  for (int i = threadIdx.x; i < (hq + hkv) * pairs; i += blockDim.x) {
+    const int h = i / pairs, j = (i % pairs) * 2;
     __nv_bfloat16* hp = row + h * D;
-    const float x1 = __bfloat162float(hp[j]), x2 = __bfloat162float(hp[j + half]);
-    const __nv_bfloat16 y1 = __float2bfloat16(x1 * cs - x2 * sn);
-    const __nv_bfloat16 y2 = __float2bfloat16(x2 * cs + x1 * sn);
-    if (h < hq) {
-      hp[j] = y1;
-      hp[j + half] = y2;
-    } else {
-      const int kh = h - hq;
-      __nv_bfloat16* dst = kv_base + (static_cast<size_t>(kh) * 16 + off) * D;
-      dst[j] = y1;
-      dst[j + half] = y2;
-    }
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(hp + j));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(hp + j + half));
+    const float2 r0 = rot[j], r1 = rot[j + 1];
+    const __nv_bfloat162 y1 = __floats2bfloat162_rn(a.x * r0.x - b.x * r0.y, a.y * r1.x - b.y * r1.y);
+    const __nv_bfloat162 y2 = __floats2bfloat162_rn(b.x * r0.x + a.x * r0.y, b.y * r1.x + a.y * r1.y);
+    __nv_bfloat16* dst = h < hq ? hp : kv_base + (static_cast<size_t>(h - hq) * 16 + off) * D;
+    *reinterpret_cast<__nv_bfloat162*>(dst + j) = y1;
+    *reinterpret_cast<__nv_bfloat162*>(dst + j + half) = y2;
   }
   // v rows: straight copy, 16 bytes per thread
   const __nv_bfloat16* v = row + (hq + hkv) * D;
@@ -197,7 +202,7 @@ void rope_append(__nv_bfloat16* qkv, const int32_t* tok_pos, const int32_t* tok_
                  int hkv, int D, int num_layers, int layer, float theta, const IterDesc* desc, int grid,
                  cudaStream_t s) {
   if (grid > 0)
-    rope_append_kernel<<<grid, 128, 0, s>>>(qkv, tok_pos, tok_slot, pool, hq, hkv, D, num_layers, layer, theta, desc);
+    rope_append_kernel<<<grid, 256, 0, s>>>(qkv, tok_pos, tok_slot, pool, hq, hkv, D, num_layers, layer, theta, desc);
 }
 
 // ---------------------------------------------------------------- argmax ----

@@ -17,8 +17,8 @@ if has tests; then timeout 900 python -m pytest tests -m gpu -x -q > "$OUT/pytes
 if has bench; then timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/bench.err"; fi
 NCU="ncu --clock-control none"
 if has launches; then
-  timeout 900 $NCU --metrics gpu__time_duration.sum -c 6000 --csv --log-file "$OUT/launches.csv" \
-    python bench.py --steps 40 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
+  CS_NO_PACING=1 timeout 900 $NCU --metrics gpu__time_duration.sum -c 20000 --csv --log-file "$OUT/launches.csv" \
+    python bench.py --steps 60 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
 fi
 if has k1; then
   timeout 600 $NCU --set full --import-source on -k regex:attn_decode_kernel -s 1 -c 1 -o "$OUT/k1_decode" -f \
