@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libconserve_b200.so")
+LIB_PATH = os.environ.get("CS_LIB_PATH") or os.path.join(_HERE, "libconserve_b200.so")  # override: experiments only
 
 CS_OK = 0
 CS_ERR_LOGIC = -1

@@ -3,30 +3,42 @@
 // oracle_latency, proj/src/perf_model.cpp:56-65).
 //
 // One CTA = two 128-row query tiles (256 packed (token, head-in-group) rows of
-// one entry) x one KV head. Keys stream in tiles of 128 (8 pages of 16
-// tokens) through a 2-stage shared-memory ring fed by TMA straight from the
+// one entry) x one KV head. Keys stream in tiles of 64 (4 pages of 16 tokens)
+// through a 4-stage shared-memory ring fed by TMA straight from the
 // block-table-indexed HBM pool (one 2D tensor map over the pool's [rows][D]
 // view; a page of one (layer, K|V, head) is 16 contiguous rows), so every K/V
 // byte loaded serves 256 query rows. Warp roles (320 threads):
-//   warp 8      TMA producer (one lane): K and V pages of key tile j -> stage j%2
-//   warp 9      MMA issuer (one lane), ping-pong over the two query tiles:
-//               S_i = Q_i K_j^T (SS, M=128 N=128 K=D) into TMEM S_i, then
-//               O_i += P_i V_j (TS: P_i read from TMEM, V_j from smem
-//               MN-major; M=128 N=D K=128) into TMEM O_i
+//   warp 8      TMA producer (one lane): K and V pages of key tile j -> stage j%4
+//   warp 9      MMA issuer (one lane): S_i(j) = Q_i K_j^T (SS, M=128 N=64 K=D)
+//               into TMEM buffer S_i[j%2] one key tile AHEAD of the softmax,
+//               and O_i += P_i(j) V_j (TS: P_i read from TMEM, V_j from smem
+//               MN-major; M=128 N=D K=64) into TMEM O_i
 //   warps 0-3   softmax/epilogue of query tile 0, warps 4-7 of tile 1; one
 //               thread per row == one TMEM lane: tcgen05.ld the S row, causal
 //               mask on absolute positions (recompute positions may be
 //               non-contiguous), online softmax with lazy rescale (O_i in TMEM
 //               is corrected only when the row max grows by > 2^8), P_i as
-//               packed bf16 written back over S_i's columns (tcgen05.st),
-//               final O_i / l to HBM.
-// While softmax i works on S_i(j), the tensor core runs the other tile's
-// S/PV, so MUFU/ALU time overlaps the UMMA time.
-// TMEM (512 cols): S_0 [0,128)  S_1 [128,256)  O_0 [256,256+D)  O_1 [384,384+D).
-// mbarriers: k_full/v_full (TMA->MMA), kv_empty (MMA->TMA, tcgen05.commit),
-// s_full_i / o_done_i (MMA->softmax i), p_full_i (softmax i -> MMA, 128 arrivals).
+//               packed bf16 written back over the S buffer's columns
+//               (tcgen05.st), final O_i / l to HBM.
+// Because S is double-buffered per query tile, the softmax of key tile j never
+// waits for the tensor core: S(j+1) is computed while P(j) is being made.
+// TMEM (512 cols): S_0 [0,64) [64,128)  S_1 [128,192) [192,256)
+//                  O_0 [256,256+D)  O_1 [384,384+D).
+// mbarriers (each waited at most one phase behind): k_full/v_full/kv_empty
+// per stage, s_full/p_full per (query tile, S buffer), o_done per query tile.
 #include "common.cuh"
 #include "tc.cuh"
+
+#ifdef CS_K2_TIMERS  // experiment builds only: per-role cycle accounting printed by one CTA
+#include <cstdio>
+#define K2T_DECL(x) long long x = 0
+#define K2T_NOW() clock64()
+#define K2T_ADD(x, t0) x += clock64() - (t0)
+#else
+#define K2T_DECL(x)
+#define K2T_NOW() 0LL
+#define K2T_ADD(x, t0)
+#endif
 
 namespace csk {
 
@@ -34,22 +46,24 @@ namespace {
 
 constexpr int kRows = 128;   // UMMA M: rows per query tile
 constexpr int kQT = 2;       // query tiles per CTA
-constexpr int kKeys = 128;   // keys per tile
+constexpr int kKeys = 64;    // keys per tile (UMMA N of S, K of PV)
+constexpr int kStages = 4;   // K/V ring depth
 constexpr int kPage = 16;
 constexpr int kThreads = 320;
-constexpr int kChunkBytes = 128 * 128;  // one [128 rows][64 bf16] SWIZZLE_128B chunk = 16 KB
+constexpr int kChunkBytes = 128 * 128;        // [128 rows][64 bf16] SWIZZLE_128B chunk (Q) = 16 KB
+constexpr int kKvChunkBytes = kKeys * 128;    // [64 keys][64 bf16] chunk (K, V) = 8 KB
 
 template <int D>
 struct TcLayout {
   static constexpr int kChunks = D / 64;
   static constexpr int q = 0;                                        // [tile][chunk]
   static constexpr int k = q + kQT * kChunks * kChunkBytes;          // [stage][chunk]
-  static constexpr int v = k + 2 * kChunks * kChunkBytes;
-  static constexpr int bar = v + 2 * kChunks * kChunkBytes;
-  static constexpr int bytes = bar + 128 + 1024;                     // barriers + 1 KB alignment slack
+  static constexpr int v = k + kStages * kChunks * kKvChunkBytes;
+  static constexpr int bar = v + kStages * kChunks * kKvChunkBytes;
+  static constexpr int bytes = bar + 256 + 1024;                     // barriers + 1 KB alignment slack
   // one CTA per SM (each allocates all 512 TMEM columns)
   static constexpr int launch_bytes = bytes < 120 * 1024 ? 120 * 1024 : bytes;
-  static constexpr int tmem_s = 0;      // + i * 128
+  static constexpr int tmem_s = 0;      // + i * 128 + buffer * 64
   static constexpr int tmem_o = 256;    // + i * 128
 };
 
@@ -83,30 +97,44 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool has2 = t.row0 + kRows < n_rows;  // second query tile present
   const int last_row = min(t.row0 + kQT * kRows, n_rows) - 1;
   const int kv_hi = min(kv_len, p.tok_pos[q0 + last_row / G] + 1);
-  const int n_kt = (kv_hi + kKeys - 1) / kKeys;
+  // split-K over key tiles (small grids over long contexts): this CTA runs
+  // key tiles [jb, jb + n_kt) of [0, ceil(kv_hi / 64))
+  const int split = blockIdx.z;
+  const int jb = split * p.k2_tiles_per_split;
+  const int n_kt = min((kv_hi + kKeys - 1) / kKeys - jb, p.k2_tiles_per_split);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  if (n_kt <= 0) {  // causal: no keys of this split reach these rows
+    if (p.k2_splits > 1) {
+      float* ws = p.ws2 + ((static_cast<size_t>(tile_idx) * p.hkv + kvh) * p.k2_splits + split) * (D + 2) * 256;
+      for (int r = threadIdx.x; r < 256; r += blockDim.x) ws[D * 256 + r] = -INFINITY;
+    }
+    return;
+  }
   uint8_t* sQ = smem + Lay::q;
   uint8_t* sK = smem + Lay::k;
   uint8_t* sV = smem + Lay::v;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::bar);
-  uint64_t* k_full = bars + 0;     // [2 stages]
-  uint64_t* v_full = bars + 2;     // [2]
-  uint64_t* kv_empty = bars + 4;   // [2]
-  uint64_t* s_full = bars + 6;     // [2 query tiles]
-  uint64_t* p_full = bars + 8;     // [2]
-  uint64_t* o_done = bars + 10;    // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* k_full = bars + 0;                   // [kStages]
+  uint64_t* v_full = k_full + kStages;           // [kStages]
+  uint64_t* kv_empty = v_full + kStages;         // [kStages]
+  uint64_t* s_full = kv_empty + kStages;         // [query tile][S buffer]
+  uint64_t* p_full = s_full + 4;                 // [query tile][S buffer]
+  uint64_t* o_done = p_full + 4;                 // [query tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kStages; ++i) {
       tc::mbar_init(&k_full[i], 1);
       tc::mbar_init(&v_full[i], 1);
       tc::mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
       tc::mbar_init(&s_full[i], 1);
       tc::mbar_init(&p_full[i], kRows);
-      tc::mbar_init(&o_done[i], 1);
     }
+    tc::mbar_init(&o_done[0], 1);
+    tc::mbar_init(&o_done[1], 1);
     tc::fence_mbar_init();
   }
   if (warp == 8 && lane == 0) tc::prefetch_tmap(&kv_map);
@@ -138,81 +166,118 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 8) {
     // ------------------------------------------------------ TMA producer --
-    if (lane == 0) {
-      constexpr uint32_t kTileBytes = CH * kChunkBytes;  // 128 keys x D bf16
+    // warp-wide loop, one elected lane issues
+    {
+      constexpr uint32_t kTileBytes = CH * kKvChunkBytes;  // 64 keys x D bf16
       for (int j = 0; j < n_kt; ++j) {
-        const int st = j & 1;
-        if (j >= 2) tc::mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
-        for (int which = 0; which < 2; ++which) {
-          uint64_t* bar = which == 0 ? &k_full[st] : &v_full[st];
-          uint8_t* dst = (which == 0 ? sK : sV) + st * CH * kChunkBytes;
-          tc::mbar_expect_tx(bar, kTileBytes);
-#pragma unroll 1
-          for (int pi = 0; pi < kKeys / kPage; ++pi) {
-            // pages past the last one reload a valid page: their keys are
-            // masked to p = 0, and finite V keeps 0 * V == 0
-            const int pg = min(j * (kKeys / kPage) + pi, n_pages - 1);
-            const int32_t row = pool_row(p, bt[pg], which, kvh);
+        const int st = j % kStages;
+        if (j >= kStages) tc::mbar_wait(&kv_empty[st], ((j / kStages) - 1) & 1);
+        // lane pi < 4 resolves page pi of the tile (pages past the last one
+        // reload a valid page: masked to p = 0, finite V keeps 0 * V == 0)
+        const int pg = min((jb + j) * (kKeys / kPage) + (lane & 3), n_pages - 1);
+        const int32_t blk = bt[pg];
+        int32_t pblk[kKeys / kPage];
 #pragma unroll
-            for (int c = 0; c < CH; ++c)
-              tc::tma_load_2d(dst + c * kChunkBytes + pi * kPage * 128, &kv_map, bar, c * 64, row);
+        for (int pi = 0; pi < kKeys / kPage; ++pi) pblk[pi] = __shfl_sync(0xffffffffu, blk, pi);
+        if (tc::elect_one_sync()) {
+          for (int which = 0; which < 2; ++which) {
+            uint64_t* bar = which == 0 ? &k_full[st] : &v_full[st];
+            uint8_t* dst = (which == 0 ? sK : sV) + st * CH * kKvChunkBytes;
+            tc::mbar_expect_tx(bar, kTileBytes);
+#pragma unroll
+            for (int pi = 0; pi < kKeys / kPage; ++pi) {
+              const int32_t row = pool_row(p, pblk[pi], which, kvh);
+#pragma unroll
+              for (int c = 0; c < CH; ++c)
+                tc::tma_load_2d(dst + c * kKvChunkBytes + pi * kPage * 128, &kv_map, bar, c * 64, row);
+            }
           }
         }
+        __syncwarp();
       }
     }
   } else if (warp == 9) {
     // -------------------------------------------------------- MMA issuer --
-    if (lane == 0) {
+    // warp-wide loop (descriptors in the uniform datapath), one elected lane
+    // issues each group of UMMAs and its commit
+    {
       constexpr uint32_t idesc_s = tc::idesc_bf16_f32(kRows, kKeys, false, false);
       constexpr uint32_t idesc_o = tc::idesc_bf16_f32(kRows, D, false, true);
       const uint32_t q_addr = tc::smem_u32(sQ), k_addr = tc::smem_u32(sK), v_addr = tc::smem_u32(sV);
       const int nq = has2 ? 2 : 1;
+      // S_i(j) -> buffer j%2; needs K_j landed
       auto issue_s = [&](int qi, int j) {
-        const uint32_t kb = k_addr + (j & 1) * CH * kChunkBytes;
+        const uint32_t kb = k_addr + (j % kStages) * CH * kKvChunkBytes;
         const uint32_t qb = q_addr + qi * CH * kChunkBytes;
+        const uint32_t d_tmem = tmem + Lay::tmem_s + qi * 128 + (j & 1) * kKeys;
+        if (tc::elect_one_sync()) {
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t off = (ks >> 2) * kChunkBytes + (ks & 3) * 32;
-          tc::umma_bf16_ss(tmem + Lay::tmem_s + qi * 128, tc::sdesc_sw128(qb + off, 16, 1024),
-                           tc::sdesc_sw128(kb + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
-        }
-        tc::umma_commit(&s_full[qi]);
-      };
-      auto issue_pv = [&](int qi, int j) {
-        const uint32_t vb = v_addr + (j & 1) * CH * kChunkBytes;
-#pragma unroll
-        for (int ks = 0; ks < kKeys / 16; ++ks) {
-          // A = P_i in TMEM (16 keys = 8 packed columns); B = V read
-          // MN-major: 16 keys = two 8-key atoms (SBO), 64-dim chunks LBO apart
-          tc::umma_bf16_ts(tmem + Lay::tmem_o + qi * 128, tmem + Lay::tmem_s + qi * 128 + ks * 8,
-                           tc::sdesc_sw128(vb + ks * 16 * 128, kChunkBytes, 1024), idesc_o,
-                           (j > 0 || ks > 0) ? 1u : 0u);
-        }
-        tc::umma_commit(&o_done[qi]);
-      };
-      tc::mbar_wait(&k_full[0], 0);
-      tc::tc_fence_after();
-      for (int qi = 0; qi < nq; ++qi) issue_s(qi, 0);
-      for (int j = 0; j < n_kt; ++j) {
-        const int st = j & 1;
-        tc::mbar_wait(&v_full[st], (j >> 1) & 1);
-        const bool next = j + 1 < n_kt;
-        for (int qi = 0; qi < nq; ++qi) {
-          tc::mbar_wait(&p_full[qi], j & 1);
-          tc::tc_fence_after();
-          issue_pv(qi, j);
-          if (qi == nq - 1) tc::umma_commit(&kv_empty[st]);  // K_j, V_j fully consumed
-          if (next) {
-            // S_i(j+1) overwrites the P_i(j) columns PV_i(j) reads: UMMAs from
-            // one thread execute in issue order
-            if (qi == 0) {
-              tc::mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-              tc::tc_fence_after();
-            }
-            issue_s(qi, j + 1);
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint32_t qoff = (ks >> 2) * kChunkBytes + (ks & 3) * 32;
+            const uint32_t koff = (ks >> 2) * kKvChunkBytes + (ks & 3) * 32;
+            tc::umma_bf16_ss(d_tmem, tc::sdesc_sw128(qb + qoff, 16, 1024), tc::sdesc_sw128(kb + koff, 16, 1024),
+                             idesc_s, ks > 0 ? 1u : 0u);
           }
+          tc::umma_commit(&s_full[qi * 2 + (j & 1)]);
+        }
+        __syncwarp();
+      };
+      // O_i += P_i(j) V_j; P_i(j) is packed bf16 in S buffer j%2
+      auto issue_pv = [&](int qi, int j, bool release_stage) {
+        const uint32_t vb = v_addr + (j % kStages) * CH * kKvChunkBytes;
+        const uint32_t pa = tmem + Lay::tmem_s + qi * 128 + (j & 1) * kKeys;
+        const uint32_t d_tmem = tmem + Lay::tmem_o + qi * 128;
+        if (tc::elect_one_sync()) {
+#pragma unroll
+          for (int ks = 0; ks < kKeys / 16; ++ks) {
+            // B = V read MN-major: 16 keys = two 8-key atoms (SBO), 64-dim
+            // chunks LBO apart
+            tc::umma_bf16_ts(d_tmem, pa + ks * 8, tc::sdesc_sw128(vb + ks * 16 * 128, kKvChunkBytes, 1024), idesc_o,
+                             (j > 0 || ks > 0) ? 1u : 0u);
+          }
+          tc::umma_commit(&o_done[qi]);
+          if (release_stage) tc::umma_commit(&kv_empty[j % kStages]);  // K_j, V_j fully consumed
+        }
+        __syncwarp();
+      };
+      K2T_DECL(t_wk);
+      K2T_DECL(t_wv);
+      K2T_DECL(t_wp);
+      const long long t_begin = K2T_NOW();
+      auto wait_k = [&](int j) {
+        const long long t0 = K2T_NOW();
+        tc::mbar_wait(&k_full[j % kStages], (j / kStages) & 1);
+        K2T_ADD(t_wk, t0);
+        tc::tc_fence_after();
+      };
+      // prologue: S(0) and S(1) for both query tiles
+      for (int j = 0; j < min(2, n_kt); ++j) {
+        wait_k(j);
+        for (int qi = 0; qi < nq; ++qi) issue_s(qi, j);
+      }
+      for (int j = 0; j < n_kt; ++j) {
+        const int st = j % kStages;
+        long long t0 = K2T_NOW();
+        tc::mbar_wait(&v_full[st], (j / kStages) & 1);
+        K2T_ADD(t_wv, t0);
+        const bool ahead = j + 2 < n_kt;
+        if (ahead) wait_k(j + 2);
+        for (int qi = 0; qi < nq; ++qi) {
+          t0 = K2T_NOW();
+          tc::mbar_wait(&p_full[qi * 2 + (j & 1)], (j >> 1) & 1);
+          K2T_ADD(t_wp, t0);
+          tc::tc_fence_after();
+          issue_pv(qi, j, qi == nq - 1);
+          // S_i(j+2) reuses buffer j%2: issued after PV_i(j), its last reader
+          // (UMMAs from one thread execute in issue order)
+          if (ahead) issue_s(qi, j + 2);
         }
       }
+#ifdef CS_K2_TIMERS
+      if (lane == 0 && blockIdx.y == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && blockIdx.z == 0)
+        printf("K2T mma  cta=%d n_kt=%d total=%lld wait_k=%lld wait_v=%lld wait_p=%lld\n", blockIdx.x, n_kt,
+               clock64() - t_begin, t_wk, t_wv, t_wp);
+#endif
     }
   } else {
     // ------------------------------------------- softmax + epilogue (rows) --
@@ -223,41 +288,45 @@ __global__ void __launch_bounds__(kThreads, 1)
       // invalid rows run the same math on the last row's position (discarded)
       const int pos = p.tok_pos[q0 + (valid ? gr : last_row) / G];
       const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-      const uint32_t ts = tmem + lane_base + Lay::tmem_s + qi * 128;
+      const uint32_t ts0 = tmem + lane_base + Lay::tmem_s + qi * 128;
       const uint32_t to = tmem + lane_base + Lay::tmem_o + qi * 128;
-      float m_used = -INFINITY, l = 0.f;
+      const float scale = p.scale_log2;
+      float m_used = -INFINITY, l = 0.f;  // m_used in scaled (log2) units
+      K2T_DECL(t_ws);
+      K2T_DECL(t_wo);
+      const long long t_sbegin = K2T_NOW();
       for (int j = 0; j < n_kt; ++j) {
-        tc::mbar_wait(&s_full[qi], j & 1);
+        const int b = j & 1;
+        const uint32_t ts = ts0 + b * kKeys;
+        const long long t0 = K2T_NOW();
+        tc::mbar_wait(&s_full[qi * 2 + b], (j >> 1) & 1);
+        K2T_ADD(t_ws, t0);
         tc::tc_fence_after();
         float s[kKeys];
 #pragma unroll
         for (int c = 0; c < kKeys / 32; ++c) tc::tmem_ld32(ts + c * 32, s + c * 32);
         tc::tmem_wait_ld();
         tc::reg_fence<kKeys>(s);
-        const int kbase = j * kKeys;
-        float mx = -INFINITY;
-        if (kbase + kKeys - 1 <= pos) {  // whole tile visible (all but the diagonal tiles)
+        const int kbase = (jb + j) * kKeys;
+        float mx = -INFINITY;  // raw (unscaled) max; scale > 0 commutes with max
+        if (kbase + kKeys - 1 > pos) {  // diagonal tile: causal mask
 #pragma unroll
-          for (int i = 0; i < kKeys; ++i) {
-            s[i] *= p.scale_log2;
-            mx = fmaxf(mx, s[i]);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < kKeys; ++i) {
-            s[i] = (kbase + i <= pos) ? s[i] * p.scale_log2 : -INFINITY;
-            mx = fmaxf(mx, s[i]);
-          }
+          for (int i = 0; i < kKeys; ++i) s[i] = (kbase + i <= pos) ? s[i] : -INFINITY;
         }
-        const float m_new = fmaxf(m_used, mx);
+#pragma unroll
+        for (int i = 0; i < kKeys; ++i) mx = fmaxf(mx, s[i]);
+        const float m_new = fmaxf(m_used, mx * scale);
         const bool rescale = m_new > m_used + 8.f;  // true on the first tile (m_used = -inf)
-        const float alpha = rescale ? exp2f(m_used - m_new) : 1.f;
+        const float alpha = rescale ? tc::ex2_approx(m_used - m_new) : 1.f;
         if (rescale) m_used = m_new;
+        // a split's rows may see no valid key yet (m_used = -inf): p = 0
+        const float msub = m_used == -INFINITY ? 0.f : m_used;
         uint32_t pk[kKeys / 2];
         float rs = 0.f;
 #pragma unroll
         for (int i = 0; i < kKeys; i += 2) {
-          const float p0 = exp2f(s[i] - m_used), p1 = exp2f(s[i + 1] - m_used);
+          const float p0 = tc::ex2_approx(fmaf(s[i], scale, -msub));
+          const float p1 = tc::ex2_approx(fmaf(s[i + 1], scale, -msub));
           rs += p0 + p1;
           pk[i / 2] = pack_bf16(p0, p1);
         }
@@ -266,7 +335,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // runs for the whole warp if any of its rows needs it (alpha = 1 for
         // the others)
         if (__any_sync(0xffffffffu, rescale) && j > 0) {
+          const long long t1 = K2T_NOW();
           tc::mbar_wait(&o_done[qi], (j - 1) & 1);  // PV_i(j-1) landed in O_i
+          K2T_ADD(t_wo, t1);
           tc::tc_fence_after();
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
@@ -279,17 +350,39 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::tmem_st32(to + c * 32, o);
           }
         }
-        // P_i(j) over S_i's first 64 columns (S_i(j) is in registers already;
-        // PV_i(j-1), the last reader of P_i(j-1), ran before S_i(j))
+        // P_i(j) over the S buffer's first 32 columns (S_i(j) is in registers;
+        // PV_i(j-2), the previous reader of this buffer, ran before S_i(j))
         tc::tmem_st32u(ts, pk);
-        tc::tmem_st32u(ts + 32, pk + 32);
         tc::tmem_wait_st();
         tc::tc_fence_before();
-        tc::mbar_arrive(&p_full[qi]);
+        tc::mbar_arrive(&p_full[qi * 2 + b]);
       }
-      // epilogue: O_i / l -> HBM
+#ifdef CS_K2_TIMERS
+      if (r == 0 && blockIdx.y == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && blockIdx.z == 0)
+        printf("K2T smax cta=%d qi=%d loop=%lld wait_s=%lld wait_o=%lld\n", blockIdx.x, qi, clock64() - t_sbegin,
+               t_ws, t_wo);
+#endif
+      // epilogue: O_i / l -> HBM (or this split's partial -> workspace).
+      // S(n_kt-1) completing only proves PV(n_kt-3) done, so step through
+      // o_done's last two phases (a parity wait must be <= 1 phase behind)
+      if (n_kt >= 2) tc::mbar_wait(&o_done[qi], (n_kt - 2) & 1);
       tc::mbar_wait(&o_done[qi], (n_kt - 1) & 1);
       tc::tc_fence_after();
+      if (p.k2_splits > 1) {
+        float* ws = p.ws2 + ((static_cast<size_t>(tile_idx) * p.hkv + kvh) * p.k2_splits + split) * (D + 2) * 256;
+        const int rr = qi * kRows + r;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          float o[32];
+          tc::tmem_ld32(to + c * 32, o);
+          tc::tmem_wait_ld();
+          tc::reg_fence<32>(o);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ws[(c * 32 + i) * 256 + rr] = o[i];
+        }
+        ws[D * 256 + rr] = l > 0.f ? m_used : -INFINITY;
+        ws[(D + 1) * 256 + rr] = l;
+      } else {
       const float inv = l > 0.f ? 1.f / l : 0.f;
       __nv_bfloat16* dst = p.out + static_cast<size_t>(q0 + (valid ? gr : 0) / G) * p.hq * D +
                            static_cast<size_t>(kvh * G + (valid ? gr : 0) % G) * D;
@@ -308,12 +401,49 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      }
     }
   }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+// Split-K merge for K2: one CTA per (tile, KV head), one thread per packed
+// row; partials are [d][row] so every load is coalesced across the rows.
+template <int D, int G>
+__global__ void __launch_bounds__(256) attn_prefill_combine_kernel(AttnParams p) {
+  const int tile = blockIdx.x, kvh = blockIdx.y;
+  if (tile >= p.desc->n_pt_cur) return;
+  const PrefillTile t = p.tiles[tile];
+  const int ent = t.entry;
+  const int gr = t.row0 + threadIdx.x;
+  if (gr >= p.ent_qlen[ent] * G) return;
+  const int S = p.k2_splits;
+  const float* ws = p.ws2 + (static_cast<size_t>(tile) * p.hkv + kvh) * S * (D + 2) * 256;
+  const int r = threadIdx.x;
+  float M = -INFINITY;
+  for (int sp = 0; sp < S; ++sp) M = fmaxf(M, ws[(sp * (D + 2) + D) * 256 + r]);
+  float w[64];  // S <= 64
+  float L = 0.f;
+  for (int sp = 0; sp < S; ++sp) {
+    const float m = ws[(sp * (D + 2) + D) * 256 + r];
+    w[sp] = m == -INFINITY ? 0.f : exp2f(m - M);
+    L += w[sp] == 0.f ? 0.f : w[sp] * ws[(sp * (D + 2) + D + 1) * 256 + r];
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  __nv_bfloat16* dst = p.out + static_cast<size_t>(p.ent_q0[ent] + gr / G) * p.hq * D +
+                       static_cast<size_t>(kvh * G + gr % G) * D;
+  for (int d = 0; d < D; d += 2) {
+    float o0 = 0.f, o1 = 0.f;
+    for (int sp = 0; sp < S; ++sp) {
+      if (w[sp] == 0.f) continue;  // skipped splits may hold stale partials
+      o0 += w[sp] * ws[(sp * (D + 2) + d) * 256 + r];
+      o1 += w[sp] * ws[(sp * (D + 2) + d + 1) * 256 + r];
+    }
+    *reinterpret_cast<uint32_t*>(dst + d) = pack_bf16(o0 * inv, o1 * inv);
+  }
 }
 
 template <int D, int G>
@@ -324,7 +454,9 @@ void launch_prefill_tc_t(const AttnParams& p, const CUtensorMap* kv_map, int n_p
                          TcLayout<D>::launch_bytes);
     attr = true;
   }
-  attn_prefill_tc_kernel<D, G><<<dim3(n_pt_grid, p.hkv), kThreads, TcLayout<D>::launch_bytes, s>>>(p, *kv_map);
+  attn_prefill_tc_kernel<D, G><<<dim3(n_pt_grid, p.hkv, p.k2_splits), kThreads, TcLayout<D>::launch_bytes, s>>>(
+      p, *kv_map);
+  if (p.k2_splits > 1) attn_prefill_combine_kernel<D, G><<<dim3(n_pt_grid, p.hkv), 256, 0, s>>>(p);
 }
 
 // Rows per K2 work tile (engine.cu builds the tile list with this step).

@@ -217,6 +217,8 @@ struct cs_engine {
   float* logits = nullptr;
   float* ws = nullptr;
   size_t ws_floats = 0;
+  float* ws2 = nullptr;  // K2 split-K partials
+  size_t ws2_floats = 0;
   uint8_t* d_meta = nullptr;
   uint8_t* h_meta = nullptr;
   size_t meta_cap = 0;
@@ -244,6 +246,7 @@ struct cs_engine {
     int n_tok = 0, n_tok_on = 0, n_ent = 0, n_ent_on = 0, n_dec = 0, n_pt = 0;
     bool has_offline = false, paced = false;
     int splits = 1, pps = 1;
+    int k2_splits = 1, k2_tps = 1 << 30;
     std::vector<cs_batch_entry> entries;
     std::vector<std::array<int64_t, 3>> writes;  // (id, w0, w1) per entry (w0<0: none)
     csk::AttnParams ap{};
@@ -439,7 +442,7 @@ void cs_engine::enqueue_layers() {
       }
     }
     launches += (l == 0 ? 1 : 0) + (is_sp(l) ? 1 : 0) + 4 + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
-                (it.n_dec > 0 ? (it.splits > 1 ? 2 : 1) : 0) + (it.n_pt > 0 ? 1 : 0);
+                (it.n_dec > 0 ? (it.splits > 1 ? 2 : 1) : 0) + (it.n_pt > 0 ? (it.k2_splits > 1 ? 2 : 1) : 0);
     if (it.paced) CK(cudaEventRecord(ev_layer[l], s_compute));
     if (cfg.flags & CS_FLAG_SYNC_DEBUG) {
       CK(cudaStreamSynchronize(s_compute));
@@ -476,7 +479,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     std::vector<int32_t> dec_ent, bt;
     std::vector<csk::PrefillTile> tiles;
     bool seen_offline = false;
-    int n_tok_on = 0, n_ent_on = 0, n_dec_on = 0, n_pt_on = 0, max_dec_pages = 0;
+    int n_tok_on = 0, n_ent_on = 0, n_dec_on = 0, n_pt_on = 0, max_dec_pages = 0, max_pre_kv = 0;
     for (int i = 0; i < n; ++i) {
       const cs_batch_entry& be = entries[i];
       if (be.online && seen_offline) throw std::invalid_argument("online entries must form a prefix of the plan");
@@ -526,6 +529,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
       } else {
         // K2 work tiles: prefill_tile_rows() packed (token, head-in-group) rows
         const int rows = static_cast<int>(pos.size()) * e->G;
+        max_pre_kv = std::max(max_pre_kv, kv_len);
         const int step = csk::prefill_tile_rows();
         for (int r0 = 0; r0 < rows; r0 += step) tiles.push_back({i, r0});
       }
@@ -617,6 +621,28 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
         CK(cudaMalloc(&e->ws, e->ws_floats * 4));
       }
     }
+    // split-K for K2 when the tile grid cannot fill the SMs (few prefill rows
+    // over a long context): splits of >= 8 key tiles (512 keys), <= 64
+    it.k2_splits = 1;
+    it.k2_tps = 1 << 30;
+    if (it.n_pt > 0) {
+      const int ctas = it.n_pt * e->hkv;
+      const int max_kt = (max_pre_kv + 63) / 64;
+      if (ctas < e->sms && max_kt >= 16) {
+        int S2 = (e->sms + ctas - 1) / ctas;
+        S2 = std::min({S2, max_kt / 8, 64});
+        if (S2 > 1) {
+          it.k2_tps = (max_kt + S2 - 1) / S2;
+          it.k2_splits = (max_kt + it.k2_tps - 1) / it.k2_tps;
+          const size_t need = static_cast<size_t>(it.n_pt) * e->hkv * it.k2_splits * (e->D + 2) * 256;
+          if (need > e->ws2_floats) {
+            if (e->ws2) CK(cudaFree(e->ws2));
+            e->ws2_floats = need * 2;
+            CK(cudaMalloc(&e->ws2, e->ws2_floats * 4));
+          }
+        }
+      }
+    }
     uint8_t* d = e->d_meta;
     csk::AttnParams& ap = it.ap;
     ap.qkv = e->qkv;
@@ -640,6 +666,9 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     ap.hkv = e->hkv;
     ap.qkv_stride = (e->hq + 2 * e->hkv) * e->D;
     ap.n_splits = it.splits;
+    ap.ws2 = e->ws2;
+    ap.k2_splits = it.k2_splits;
+    ap.k2_tiles_per_split = it.k2_tps;
     ap.pages_per_split = it.pps;
     ap.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(e->D));
     it.meta_bytes = static_cast<int64_t>(total);
@@ -884,7 +913,8 @@ int cs_destroy(cs_engine* e) {
       for (void* p : {static_cast<void*>(e->x), static_cast<void*>(e->xn), static_cast<void*>(e->qkv),
                       static_cast<void*>(e->attn), static_cast<void*>(e->tmp), static_cast<void*>(e->gu),
                       static_cast<void*>(e->act), static_cast<void*>(e->xl), static_cast<void*>(e->logits),
-                      static_cast<void*>(e->ws), static_cast<void*>(e->d_meta), static_cast<void*>(e->d_out),
+                      static_cast<void*>(e->ws), static_cast<void*>(e->ws2), static_cast<void*>(e->d_meta),
+                      static_cast<void*>(e->d_out),
                       e->blas_ws})
         if (p) cudaFree(p);
       if (e->h_meta) cudaFreeHost(e->h_meta);

@@ -128,3 +128,26 @@ def test_k2_lazy_rescale_path():
         _check_rows(eng, [e], [list(range(600, 900))], 300)
     finally:
         eng.close()
+
+
+def test_k2_split_k_small_chunks_over_long_context():
+    """Few prefill rows over a long context launch fewer CTAs than SMs: K2
+    splits the key range (split-K + merge), including splits that hold no
+    visible key for a short entry (empty partials)."""
+    eng = _engine()
+    try:
+        eng.register_request(0, False)
+        eng.register_request(1, False)
+        eng.register_request(2, True)
+        _run(eng, [cs.BatchEntry(0, 4000, 0, cs.CS_PREFILL, False)], [4000])
+        e_on = cs.BatchEntry(2, 30, 0, cs.CS_PREFILL, True)        # short: 1 key tile
+        e_long = cs.BatchEntry(0, 20, 4000, cs.CS_PREFILL, False)  # 20 rows over 4020 keys
+        _run(eng, [e_on, e_long], [30, 20])
+        _check_rows(eng, [e_on, e_long], [list(range(30)), list(range(4000, 4020))], 50)
+        e3 = cs.BatchEntry(1, 700, 0, cs.CS_PREFILL, False)
+        _run(eng, [e3], [700])
+        e4 = cs.BatchEntry(0, 40, 4020, cs.CS_PREFILL, False)
+        _run(eng, [e4], [40])
+        _check_rows(eng, [e4], [list(range(4020, 4060))], 40)
+    finally:
+        eng.close()

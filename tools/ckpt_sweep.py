@@ -33,7 +33,7 @@ from paper_2410_01228_b200 import _ffi as F  # noqa: E402
 
 def _engine(n_blocks: int, tp: int):
     page = 16 * 131072
-    cfg = cs.model_config("llama8b", flags=F.CS_FLAG_NO_MODEL, gpu_kv_capacity=(n_blocks + 8) * page,
+    cfg = cs.model_config("llama8b", flags=F.CS_FLAG_NO_MODEL | F.CS_FLAG_NO_FWD_QUARANTINE, gpu_kv_capacity=(n_blocks + 8) * page,
                           host_kv_capacity=(n_blocks + 8) * page, max_entries=64, extra_blocks=64,
                           extra_host_slots=64, tp_size=tp, tp_rank=0)
     return cs.Engine(cfg)
