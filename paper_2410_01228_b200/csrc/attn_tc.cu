@@ -31,10 +31,26 @@
 
 #ifdef CS_K2_TIMERS  // experiment builds only: per-role cycle accounting printed by one CTA
 #include <cstdio>
+// bounded wait: reports (tag, j, parity, CTA) and traps instead of hanging
+#define K2_WAIT(bar, par, tag, jj)                                                                          \
+  do {                                                                                                      \
+    uint32_t ok_ = 0;                                                                                       \
+    for (long it_ = 0; it_ < 20000000 && !ok_; ++it_) {                                                     \
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"        \
+                   "selp.b32 %0, 1, 0, p;\n\t}"                                                          \
+                   : "=r"(ok_) : "r"(tc::smem_u32(bar)), "r"(par) : "memory");                              \
+    }                                                                                                       \
+    if (!ok_) {                                                                                             \
+      printf("K2 HANG %s j=%d par=%d n_kt=%d cta=(%d,%d,%d) tid=%d\n", tag, (int)(jj), (int)(par), n_kt,  \
+             blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x);                                             \
+      asm volatile("trap;");                                                                                \
+    }                                                                                                       \
+  } while (0)
 #define K2T_DECL(x) long long x = 0
 #define K2T_NOW() clock64()
 #define K2T_ADD(x, t0) x += clock64() - (t0)
 #else
+#define K2_WAIT(bar, par, tag, jj) tc::mbar_wait(bar, par)
 #define K2T_DECL(x)
 #define K2T_NOW() 0LL
 #define K2T_ADD(x, t0)
@@ -120,8 +136,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* kv_empty = v_full + kStages;         // [kStages]
   uint64_t* s_full = kv_empty + kStages;         // [query tile][S buffer]
   uint64_t* p_full = s_full + 4;                 // [query tile][S buffer]
-  uint64_t* o_done = p_full + 4;                 // [query tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* o_done = p_full + 4;                 // [query tile] once per PV
+  uint64_t* o_final = o_done + 2;                // [query tile] after the last PV
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 2);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
@@ -133,8 +150,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_init(&s_full[i], 1);
       tc::mbar_init(&p_full[i], kRows);
     }
-    tc::mbar_init(&o_done[0], 1);
-    tc::mbar_init(&o_done[1], 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&o_done[i], 1);
+      tc::mbar_init(&o_final[i], 1);
+    }
     tc::fence_mbar_init();
   }
   if (warp == 8 && lane == 0) tc::prefetch_tmap(&kv_map);
@@ -171,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t kTileBytes = CH * kKvChunkBytes;  // 64 keys x D bf16
       for (int j = 0; j < n_kt; ++j) {
         const int st = j % kStages;
-        if (j >= kStages) tc::mbar_wait(&kv_empty[st], ((j / kStages) - 1) & 1);
+        if (j >= kStages) K2_WAIT(&kv_empty[st], ((j / kStages) - 1) & 1, "kv_empty", j);
         // lane pi < 4 resolves page pi of the tile (pages past the last one
         // reload a valid page: masked to p = 0, finite V keeps 0 * V == 0)
         const int pg = min((jb + j) * (kKeys / kPage) + (lane & 3), n_pages - 1);
@@ -236,6 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                              (j > 0 || ks > 0) ? 1u : 0u);
           }
           tc::umma_commit(&o_done[qi]);
+          if (j == n_kt - 1) tc::umma_commit(&o_final[qi]);
           if (release_stage) tc::umma_commit(&kv_empty[j % kStages]);  // K_j, V_j fully consumed
         }
         __syncwarp();
@@ -246,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long t_begin = K2T_NOW();
       auto wait_k = [&](int j) {
         const long long t0 = K2T_NOW();
-        tc::mbar_wait(&k_full[j % kStages], (j / kStages) & 1);
+        K2_WAIT(&k_full[j % kStages], (j / kStages) & 1, "k_full", j);
         K2T_ADD(t_wk, t0);
         tc::tc_fence_after();
       };
@@ -258,13 +278,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < n_kt; ++j) {
         const int st = j % kStages;
         long long t0 = K2T_NOW();
-        tc::mbar_wait(&v_full[st], (j / kStages) & 1);
+        K2_WAIT(&v_full[st], (j / kStages) & 1, "v_full", j);
         K2T_ADD(t_wv, t0);
         const bool ahead = j + 2 < n_kt;
         if (ahead) wait_k(j + 2);
         for (int qi = 0; qi < nq; ++qi) {
           t0 = K2T_NOW();
-          tc::mbar_wait(&p_full[qi * 2 + (j & 1)], (j >> 1) & 1);
+          K2_WAIT(&p_full[qi * 2 + (j & 1)], (j >> 1) & 1, "p_full", j);
           K2T_ADD(t_wp, t0);
           tc::tc_fence_after();
           issue_pv(qi, j, qi == nq - 1);
@@ -299,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int b = j & 1;
         const uint32_t ts = ts0 + b * kKeys;
         const long long t0 = K2T_NOW();
-        tc::mbar_wait(&s_full[qi * 2 + b], (j >> 1) & 1);
+        K2_WAIT(&s_full[qi * 2 + b], (j >> 1) & 1, "s_full", j);
         K2T_ADD(t_ws, t0);
         tc::tc_fence_after();
         float s[kKeys];
@@ -336,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the others)
         if (__any_sync(0xffffffffu, rescale) && j > 0) {
           const long long t1 = K2T_NOW();
-          tc::mbar_wait(&o_done[qi], (j - 1) & 1);  // PV_i(j-1) landed in O_i
+          K2_WAIT(&o_done[qi], (j - 1) & 1, "o_done_rescale", j);  // PV_i(j-1) landed in O_i
           K2T_ADD(t_wo, t1);
           tc::tc_fence_after();
 #pragma unroll
@@ -363,10 +383,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                t_ws, t_wo);
 #endif
       // epilogue: O_i / l -> HBM (or this split's partial -> workspace).
-      // S(n_kt-1) completing only proves PV(n_kt-3) done, so step through
-      // o_done's last two phases (a parity wait must be <= 1 phase behind)
-      if (n_kt >= 2) tc::mbar_wait(&o_done[qi], (n_kt - 2) & 1);
-      tc::mbar_wait(&o_done[qi], (n_kt - 1) & 1);
+      // o_done may be 0..2 phases ahead here (parity-ambiguous): the last PV
+      // signals its own barrier
+      K2_WAIT(&o_final[qi], 0, "o_final", n_kt);
       tc::tc_fence_after();
       if (p.k2_splits > 1) {
         float* ws = p.ws2 + ((static_cast<size_t>(tile_idx) * p.hkv + kvh) * p.k2_splits + split) * (D + 2) * 256;

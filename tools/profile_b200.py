@@ -31,6 +31,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "b200_profile.json"))
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--p-values", type=int, nargs="*", default=list(P_VALUES))
+    ap.add_argument("--c-values", type=int, nargs="*", default=list(C_VALUES))
     args = ap.parse_args()
     cfg = cs.model_config("llama8b", gpu_kv_capacity=12 << 30, host_kv_capacity=1 << 30, max_batched_tokens=8192,
                           instrumented=0, max_entries=64)
@@ -38,7 +40,7 @@ def main():
     grid = []
     rid = 0
     try:
-        for c in C_VALUES:
+        for c in args.c_values:
             # context of c tokens, written once (its values do not change timing)
             ctx_id = None
             if c > 0:
@@ -47,7 +49,7 @@ def main():
                 eng.register_request(ctx_id, False)
                 assert eng.allocate(ctx_id, c).ok
                 eng.commit_allocations(ctx_id)
-            for p in P_VALUES:
+            for p in args.p_values:
                 times = []
                 for rep in range(args.reps + 1):
                     if ctx_id is None:
