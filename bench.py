@@ -330,6 +330,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-probes", action="store_true")
+    ap.add_argument("--dump", default=None, help="write per-iteration device times + plan shapes (.npz)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -401,6 +402,15 @@ def main():
                  "online_p99_tpot_ms": percentile(o["tpot"], 0.99), "online_p99_tbt_ms": percentile(o["tbt"], 0.99),
                  "offline_tokens": o["off"], "steps": int(o["res"].iterations)}
     tr, K, res, s0, s1 = rp["tr"], rp["K"], rp["res"], rp["s0"], rp["s1"]
+    if args.dump and rank == 0:
+        shapes = []
+        for k in range(W, W + K):
+            pl = tr.plan_of[k]
+            pre = pl[pl[:, 3] != 1]
+            dec = pl[pl[:, 3] == 1]
+            shapes.append([len(pl), int(pre[:, 1].sum()), int((pre[:, 1] * (pre[:, 1] + pre[:, 2])).sum()),
+                           len(dec), int(dec[:, 2].sum())])
+        np.savez(args.dump, gpu_ms=res.gpu_ms, wall_end_ms=res.wall_end_ms, shapes=np.array(shapes, np.int64))
     off, on, tpot, tbt = rp["off"], rp["on"], rp["tpot"], rp["tbt"]
     gpu_s, wall_s, clocks, setup_s = rp["gpu_s"], rp["wall_s"], rp["clocks"], rp["setup_s"]
     n = world
