@@ -49,15 +49,19 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
   constexpr int PB = kPage * D * 2;  // bytes per K (or V) page
   extern __shared__ __align__(128) uint8_t smem[];
   const int split = blockIdx.x, kvh = blockIdx.y, di = blockIdx.z;
-  if (di >= p.desc->n_dec_cur) return;
+  // split count and size live in the device descriptor so a captured graph
+  // (grid sized for the bucket) serves every plan of its bucket
+  const int S = p.desc->dec_splits;
+  if (di >= p.desc->n_dec_cur || split >= S) return;
+  const int pps = p.desc->dec_pps;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int ent = p.dec_ent[di];
   const int row = p.ent_q0[ent];
   const int kv_len = p.ent_kvlen[ent];
   const int n_pages = (kv_len + kPage - 1) / kPage;
-  const int pg0 = split * p.pages_per_split;
-  const int pg1 = min(n_pages, pg0 + p.pages_per_split);
+  const int pg0 = split * pps;
+  const int pg1 = min(n_pages, pg0 + pps);
   const int32_t* bt = p.block_table + p.ent_bt[ent];
 
   uint32_t qa[KS][4];
@@ -187,8 +191,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
     sm_o[(warp * 16 + gid + 8) * D + d + 1] = o[nt][3];
   }
   __syncthreads();
-  const int S = p.n_splits;
-  const size_t item = (static_cast<size_t>(di) * p.hkv + kvh) * S + split;
+  const int SG = gridDim.x;  // workspace stride (launch grid)
+  const size_t item = (static_cast<size_t>(di) * p.hkv + kvh) * SG + split;
   for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
     const int r = idx / D, d = idx % D;
     float M = -INFINITY;
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
           __float2bfloat16(L > 0.f ? O / L : 0.f);
     } else {
       float* wm = p.ws + item * G * 2;
-      float* wo = p.ws + static_cast<size_t>(gridDim.z) * p.hkv * S * G * 2 + item * G * D;
+      float* wo = p.ws + static_cast<size_t>(gridDim.z) * p.hkv * SG * G * 2 + item * G * D;
       if (d == 0) {
         wm[r * 2] = M;
         wm[r * 2 + 1] = L;
@@ -227,13 +231,14 @@ __global__ void __launch_bounds__(256) attn_decode_combine_kernel(AttnParams p, 
   __shared__ float wgt[kMaxSplits * G];  // exp2(m_s - M) per (split, row)
   __shared__ float inv_l[G];
   const int kvh = blockIdx.y, di = blockIdx.x;
-  if (di >= p.desc->n_dec_cur) return;
-  const int S = p.n_splits;
+  const int S = p.desc->dec_splits;
+  if (di >= p.desc->n_dec_cur || S <= 1) return;  // S == 1: K1 wrote the output
+  const int SG = p.n_splits;                      // workspace stride (K1 grid.x)
   const int ent = p.dec_ent[di];
   const int row = p.ent_q0[ent];
-  const size_t base_item = (static_cast<size_t>(di) * p.hkv + kvh) * S;
+  const size_t base_item = (static_cast<size_t>(di) * p.hkv + kvh) * SG;
   const float* wm = p.ws + base_item * G * 2;
-  const float* wo = p.ws + static_cast<size_t>(n_dec_grid) * p.hkv * S * G * 2 + base_item * G * D;
+  const float* wo = p.ws + static_cast<size_t>(n_dec_grid) * p.hkv * SG * G * 2 + base_item * G * D;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int r = warp; r < G; r += blockDim.x >> 5) {
     float M = -INFINITY;

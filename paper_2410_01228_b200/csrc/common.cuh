@@ -18,6 +18,8 @@ struct IterDesc {
   int32_t n_dec_cur, n_dec_all, n_dec_on;      // single-query attention rows
   int32_t n_pt_cur, n_pt_all, n_pt_on;         // prefill attention tiles
   int32_t dropped_at;                          // layer of the drop, -1 if none
+  int32_t dec_splits;                          // K1 split-K: active splits (<= launch grid.x)
+  int32_t dec_pps;                             // K1 split-K: pages per split
   int32_t pad0;
   uint64_t epoch;
   uint64_t drop_ns;                            // %globaltimer at the drop

@@ -247,6 +247,8 @@ struct cs_engine {
     bool has_offline = false, paced = false;
     int splits = 1, pps = 1;
     int k2_splits = 1, k2_tps = 1 << 30;
+    bool graph = false;  // decode-only plan replayed from a captured CUDA graph
+    int bucket = 0;      // graph bucket: token rows / entries / decode rows (padded)
     std::vector<cs_batch_entry> entries;
     std::vector<std::array<int64_t, 3>> writes;  // (id, w0, w1) per entry (w0<0: none)
     csk::AttnParams ap{};
@@ -267,6 +269,21 @@ struct cs_engine {
 
   int64_t layer_gemm_rows(int layer);
   void enqueue_layers();
+  int enqueue_body(int Tg, int Eg, bool graph);
+  // CUDA graphs of decode-only forwards, keyed by (bucket, safepoints, gen);
+  // gen bumps whenever a buffer baked into the graphs is reallocated
+  struct GraphExec {
+    cudaGraphExec_t exec = nullptr;
+    int launches = 0;
+  };
+  std::map<uint64_t, GraphExec> graphs;
+  uint64_t graph_gen = 0;
+  bool graphs_enabled = true;
+  void drop_graphs() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
+    ++graph_gen;
+  }
   void gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
   void allreduce(__nv_bfloat16* buf, int64_t count);
 };
@@ -383,20 +400,22 @@ int64_t cs_engine::layer_gemm_rows(int layer) {
   return it.n_tok;
 }
 
-// Enqueues every layer of the current iteration (caller or worker thread).
-void cs_engine::enqueue_layers() {
+// Enqueues the layer stack and the head for Tg token rows / Eg entries (the
+// plan's counts, or the graph bucket's); returns the kernels it launched.
+int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
+  int n_launch = 0;
   const auto* desc = reinterpret_cast<const csk::IterDesc*>(d_meta);
   auto* desc_mut = reinterpret_cast<csk::IterDesc*>(d_meta);
   const int lookahead = cfg.layer_lookahead > 0 ? cfg.layer_lookahead : 2;
   const bool instrumented = cfg.instrumented != 0 && it.has_offline;
   const int qkv_cols = (hq + 2 * hkv) * D;
-  const int T = it.n_tok;
+  const int T = Tg;
   __nv_bfloat16* tail = tmp + static_cast<size_t>(max_tok) * hidden;  // vote slot
   auto is_sp = [&](int l) { return instrumented && l > 0 && l < L && l % cfg.safepoint_interval_layers == 0; };
 
   for (int l = 0; l < L; ++l) {
     if (it.paced && l > lookahead) CK(cudaEventSynchronize(ev_layer[l - lookahead - 1]));
-    if (is_sp(l)) {
+    if (is_sp(l) && !graph) {
       // Host view of the flag: once seen, later layers' GEMMs shrink to the
       // online rows (the device truncates everything else at this layer).
       if (tp == 1) {
@@ -407,7 +426,7 @@ void cs_engine::enqueue_layers() {
         it.gemm_trunc_layer = l;
       }
     }
-    const int64_t M = layer_gemm_rows(l);
+    const int64_t M = graph ? Tg : layer_gemm_rows(l);
     if (l == 0) {
       csk::embed(x, w.emb, it.d_tok_ids, hidden, desc, T, s_compute);
     }
@@ -424,7 +443,7 @@ void cs_engine::enqueue_layers() {
                      cfg.rope_theta, desc, T, s_compute);
     csk::AttnParams ap = it.ap;
     ap.layer = l;
-    if (!csk::launch_attention(ap, &kv_map, D, G, it.n_dec, it.n_pt, s_compute))
+    if (!csk::launch_attention(ap, &kv_map, D, G, graph ? Tg : it.n_dec, it.n_pt, s_compute))
       throw ConfigError("unsupported attention shape");
     gemm(attn, w.wo[l], tmp, static_cast<int>(M), hidden, hq * D, false);
     allreduce(tmp, M * hidden);
@@ -441,22 +460,56 @@ void cs_engine::enqueue_layers() {
         allreduce(tmp, M * hidden);
       }
     }
-    launches += (l == 0 ? 1 : 0) + (is_sp(l) ? 1 : 0) + 4 + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
+    n_launch += (l == 0 ? 1 : 0) + (is_sp(l) ? 1 : 0) + 4 + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
                 (it.n_dec > 0 ? (it.splits > 1 ? 2 : 1) : 0) + (it.n_pt > 0 ? (it.k2_splits > 1 ? 2 : 1) : 0);
     if (it.paced) CK(cudaEventRecord(ev_layer[l], s_compute));
-    if (cfg.flags & CS_FLAG_SYNC_DEBUG) {
+    if ((cfg.flags & CS_FLAG_SYNC_DEBUG) && !graph) {
       CK(cudaStreamSynchronize(s_compute));
       CK(cudaGetLastError());
     }
   }
   // Final norm of each entry's last row -> lm_head -> argmax.
-  const int E = it.n_ent;
+  const int E = Eg;
   csk::add_rmsnorm(x, tmp, w.final_norm, xl, hidden, cfg.rms_eps, desc, it.d_ent_last, E, s_compute);
   gemm(xl, w.lm_head, logits, E, vocab, hidden, true);
   csk::argmax_rows(logits, vocab, reinterpret_cast<int32_t*>(d_out + sizeof(csk::IterDesc)), desc, E, s_compute);
   CK(cudaMemcpyAsync(d_out, d_meta, sizeof(csk::IterDesc), cudaMemcpyDeviceToDevice, s_compute));
   CK(cudaMemcpyAsync(h_out, d_out, sizeof(csk::IterDesc) + sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s_compute));
-  launches += 2;
+  n_launch += 2;
+  return n_launch;
+}
+
+// Enqueues every layer of the current iteration (caller or worker thread).
+// Decode-only plans run a CUDA graph captured once per bucket: all per-plan
+// data (counts, split sizes, block tables) is read from the device metadata,
+// so one graph serves every plan of its bucket and the ~350 launches of a
+// decode step cost one cudaGraphLaunch.
+void cs_engine::enqueue_layers() {
+  if (it.graph) {
+    const bool sp = cfg.instrumented != 0 && it.has_offline && L > 1;
+    const uint64_t key = static_cast<uint64_t>(it.bucket) | (static_cast<uint64_t>(sp) << 16) | (graph_gen << 20);
+    auto f = graphs.find(key);
+    if (f == graphs.end()) {
+      GraphExec ge;
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(s_compute, cudaStreamCaptureModeThreadLocal));
+      try {
+        ge.launches = enqueue_body(it.bucket, it.bucket, true);
+      } catch (...) {
+        cudaStreamEndCapture(s_compute, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      CK(cudaStreamEndCapture(s_compute, &g));
+      CK(cudaGraphInstantiate(&ge.exec, g, 0));
+      CK(cudaGraphDestroy(g));
+      f = graphs.emplace(key, ge).first;
+    }
+    CK(cudaGraphLaunch(f->second.exec, s_compute));
+    launches += f->second.launches;
+  } else {
+    launches += enqueue_body(it.n_tok, it.n_ent, false);
+  }
   CK(cudaEventRecord(ev_end, s_compute));
   CK(cudaEventRecord(ev_fwd_done, s_compute));
   CK(cudaGetLastError());
@@ -556,6 +609,51 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
       return false;
     }
 
+    // ---- graph mode: decode-only plans of <= 256 rows replay a captured
+    // CUDA graph of their bucket (sizes padded; kernels skip rows >= *_cur)
+    static const bool no_graphs = [] {
+      const char* v = std::getenv("CS_NO_GRAPHS");
+      return v && v[0] == '1';
+    }();
+    it.graph = false;
+    it.bucket = 0;
+    if (e->graphs_enabled && !no_graphs && it.n_pt == 0 && it.n_dec == T && T <= 256) {
+      int b = 8;
+      while (b < T) b *= 2;
+      if (b <= e->max_ent && b <= e->max_tok) {
+        it.graph = true;
+        it.bucket = b;
+      }
+    }
+    const int Tcap = it.graph ? it.bucket : T;  // token-array stride
+    const int Dcap = it.graph ? it.bucket : it.n_dec;
+
+    // ---- split-K for K1: aim for ~4 CTAs per SM. The launch grid (and the
+    // workspace stride) is SG; the active split count lives in the descriptor.
+    int SG = 1, S = 1, pps = std::max(1, max_dec_pages);
+    if (it.n_dec > 0) {
+      const int target = 4 * e->sms;
+      S = std::max(1, (target + it.n_dec * e->hkv - 1) / (it.n_dec * e->hkv));
+      S = std::min(S, std::max(1, (max_dec_pages + 3) / 4));
+      S = std::min(S, 128);  // attn_decode_combine_kernel stages <= 128 splits
+      if (it.graph) {
+        SG = std::min(128, std::max(1, (target + Dcap * e->hkv - 1) / (Dcap * e->hkv)));
+        S = std::min(S, SG);
+      }
+      pps = (max_dec_pages + S - 1) / S;
+      S = (max_dec_pages + pps - 1) / pps;
+      if (!it.graph) SG = S;
+      const size_t need = static_cast<size_t>(Dcap) * e->hkv * SG * e->G * (2 + e->D);
+      if (SG > 1 && need > e->ws_floats) {
+        if (e->ws) CK(cudaFree(e->ws));
+        e->ws_floats = need * 2;
+        CK(cudaMalloc(&e->ws, e->ws_floats * 4));
+        e->drop_graphs();
+      }
+    }
+    it.splits = SG;
+    it.pps = pps;
+
     // ---- pack metadata: [desc | tok_ids | tok_pos | tok_slot | ent x5 (cap max_ent) | dec | tiles | bt] ----
     const size_t E = static_cast<size_t>(e->max_ent);
     size_t off = 0;
@@ -565,9 +663,9 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
       return o;
     };
     const size_t o_desc = region(sizeof(csk::IterDesc));
-    const size_t o_tok = region(sizeof(int32_t) * 3 * static_cast<size_t>(T));
+    const size_t o_tok = region(sizeof(int32_t) * 3 * static_cast<size_t>(Tcap));
     const size_t o_ent = region(sizeof(int32_t) * 5 * E);
-    const size_t o_dec = region(sizeof(int32_t) * dec_ent.size() + 4);
+    const size_t o_dec = region(sizeof(int32_t) * static_cast<size_t>(Dcap) + 4);
     const size_t o_tiles = region(sizeof(csk::PrefillTile) * tiles.size() + 8);
     const size_t o_bt = region(sizeof(int32_t) * bt.size() + 4);
     const size_t total = off;
@@ -577,6 +675,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
       e->meta_cap = align_up(total * 2, 1 << 20);
       CK(cudaMalloc(&e->d_meta, e->meta_cap));
       CK(cudaMallocHost(&e->h_meta, e->meta_cap));
+      e->drop_graphs();
     }
     uint8_t* h = e->h_meta;
     csk::IterDesc desc{};
@@ -589,12 +688,14 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     desc.n_pt_cur = desc.n_pt_all = it.n_pt;
     desc.n_pt_on = n_pt_on;
     desc.dropped_at = -1;
+    desc.dec_splits = S;
+    desc.dec_pps = pps;
     desc.epoch = epoch;
     std::memcpy(h + o_desc, &desc, sizeof(desc));
     int32_t* ht = reinterpret_cast<int32_t*>(h + o_tok);
     std::memcpy(ht, tok_ids.data(), 4 * T);
-    std::memcpy(ht + T, tok_pos.data(), 4 * T);
-    std::memcpy(ht + 2 * T, tok_slot.data(), 4 * T);
+    std::memcpy(ht + Tcap, tok_pos.data(), 4 * T);
+    std::memcpy(ht + 2 * Tcap, tok_slot.data(), 4 * T);
     int32_t* he = reinterpret_cast<int32_t*>(h + o_ent);
     std::memcpy(he, ent_q0.data(), 4 * n);
     std::memcpy(he + E, ent_qlen.data(), 4 * n);
@@ -605,22 +706,6 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     if (!tiles.empty()) std::memcpy(h + o_tiles, tiles.data(), sizeof(csk::PrefillTile) * tiles.size());
     std::memcpy(h + o_bt, bt.data(), 4 * bt.size());
 
-    // split-K for K1: aim for ~4 CTAs per SM
-    if (it.n_dec > 0) {
-      const int base = it.n_dec * e->hkv;
-      const int target = 4 * e->sms;
-      int S = std::max(1, (target + base - 1) / base);
-      S = std::min(S, std::max(1, (max_dec_pages + 3) / 4));
-      S = std::min(S, 128);  // attn_decode_combine_kernel stages <= 128 splits
-      it.pps = (max_dec_pages + S - 1) / S;
-      it.splits = (max_dec_pages + it.pps - 1) / it.pps;
-      const size_t need = static_cast<size_t>(it.n_dec) * e->hkv * it.splits * e->G * (2 + e->D);
-      if (it.splits > 1 && need > e->ws_floats) {
-        if (e->ws) CK(cudaFree(e->ws));
-        e->ws_floats = need * 2;
-        CK(cudaMalloc(&e->ws, e->ws_floats * 4));
-      }
-    }
     // split-K for K2 when the tile grid cannot fill the SMs (few prefill rows
     // over a long context): splits of >= 8 key tiles (512 keys), <= 64
     it.k2_splits = 1;
@@ -639,6 +724,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
             if (e->ws2) CK(cudaFree(e->ws2));
             e->ws2_floats = need * 2;
             CK(cudaMalloc(&e->ws2, e->ws2_floats * 4));
+            e->drop_graphs();
           }
         }
       }
@@ -650,8 +736,8 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     ap.pool = e->kv;
     ap.desc = reinterpret_cast<const csk::IterDesc*>(d + o_desc);
     it.d_tok_ids = reinterpret_cast<const int32_t*>(d + o_tok);
-    ap.tok_pos = it.d_tok_ids + T;
-    it.d_tok_slot = it.d_tok_ids + 2 * T;
+    ap.tok_pos = it.d_tok_ids + Tcap;
+    it.d_tok_slot = it.d_tok_ids + 2 * Tcap;
     it.d_ent_last = reinterpret_cast<const int32_t*>(d + o_ent) + 4 * E;
     ap.ent_q0 = reinterpret_cast<const int32_t*>(d + o_ent);
     ap.ent_qlen = ap.ent_q0 + E;
@@ -901,6 +987,7 @@ int cs_destroy(cs_engine* e) {
     if (e->worker.joinable()) e->worker.join();
     if (!e->host_only) {
       cudaDeviceSynchronize();
+      e->drop_graphs();
       e->mover.reset();
       for (auto& r : e->ring) r.live.clear();
       if (e->blas) cublasDestroy(e->blas);
@@ -1103,7 +1190,7 @@ int cs_forward_launch(cs_engine* e, const cs_batch_entry* entries, int32_t n, ui
       const char* v = std::getenv("CS_NO_PACING");
       return v && v[0] == '1';
     }();
-    it.paced = e->cfg.instrumented != 0 && it.has_offline && e->L > 1 && !no_pacing;
+    it.paced = e->cfg.instrumented != 0 && it.has_offline && e->L > 1 && !no_pacing && !it.graph;
     if (!it.paced) {
       e->enqueue_layers();
       return;
