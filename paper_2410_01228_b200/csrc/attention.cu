@@ -220,37 +220,33 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
       wo[r * D + d] = O;
     }
   }
-}
-
-// Split-K merge for K1: one CTA per (entry, KV head). The per-split (max,
-// sum) pairs are staged once in shared memory with the merge weights, then
-// every thread sums its (row, dim) over the splits with independent loads.
-template <int D, int G>
-__global__ void __launch_bounds__(256) attn_decode_combine_kernel(AttnParams p, int n_dec_grid) {
-  constexpr int kMaxSplits = 128;
-  __shared__ float wgt[kMaxSplits * G];  // exp2(m_s - M) per (split, row)
-  __shared__ float inv_l[G];
-  const int kvh = blockIdx.y, di = blockIdx.x;
-  const int S = p.desc->dec_splits;
-  if (di >= p.desc->n_dec_cur || S <= 1) return;  // S == 1: K1 wrote the output
-  const int SG = p.n_splits;                      // workspace stride (K1 grid.x)
-  const int ent = p.dec_ent[di];
-  const int row = p.ent_q0[ent];
+  if (S == 1) return;
+  // Split-K merge, fused: the last CTA of this (entry, KV head) to finish
+  // folds all S partials (no separate combine launch) and re-arms the counter.
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  int32_t* cnt = p.dec_cnt + static_cast<size_t>(di) * p.hkv + kvh;
+  if (threadIdx.x == 0) s_last = atomicAdd(cnt, 1) == S - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  float* wgt = sm_m;         // [S][G] merge weights (smem reused: >= 128*8 floats)
+  float* inv_l = sm_m + S * G;
   const size_t base_item = (static_cast<size_t>(di) * p.hkv + kvh) * SG;
   const float* wm = p.ws + base_item * G * 2;
-  const float* wo = p.ws + static_cast<size_t>(n_dec_grid) * p.hkv * SG * G * 2 + base_item * G * D;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int r = warp; r < G; r += blockDim.x >> 5) {
+  const float* wo = p.ws + static_cast<size_t>(gridDim.z) * p.hkv * SG * G * 2 + base_item * G * D;
+  for (int r = warp; r < G; r += 4) {
     float M = -INFINITY;
-    for (int s = lane; s < S; s += 32) M = fmaxf(M, wm[(s * G + r) * 2]);
+    for (int sp = lane; sp < S; sp += 32) M = fmaxf(M, __ldcg(wm + (sp * G + r) * 2));
 #pragma unroll
     for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float L = 0.f;
-    for (int s = lane; s < S; s += 32) {
-      const float ms = wm[(s * G + r) * 2];
+    for (int sp = lane; sp < S; sp += 32) {
+      const float ms = __ldcg(wm + (sp * G + r) * 2);
       const float f = (M == -INFINITY || ms == -INFINITY) ? 0.f : exp2f(ms - M);
-      wgt[s * G + r] = f;
-      L += wm[(s * G + r) * 2 + 1] * f;
+      wgt[sp * G + r] = f;
+      L += __ldcg(wm + (sp * G + r) * 2 + 1) * f;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
@@ -261,10 +257,11 @@ __global__ void __launch_bounds__(256) attn_decode_combine_kernel(AttnParams p, 
     const int r = idx / D, d = idx % D;
     float O = 0.f;
 #pragma unroll 8
-    for (int s = 0; s < S; ++s) O += wo[(s * G + r) * D + d] * wgt[s * G + r];
+    for (int sp = 0; sp < S; ++sp) O += __ldcg(wo + (sp * G + r) * D + d) * wgt[sp * G + r];
     p.out[static_cast<size_t>(row) * p.hq * D + static_cast<size_t>(kvh * G + r) * D + d] =
         __float2bfloat16(O * inv_l[r]);
   }
+  if (threadIdx.x == 0) *cnt = 0;
 }
 
 // ------------------------------------------------------------- launchers ----
@@ -285,7 +282,6 @@ static void launch_attention_t(const AttnParams& p, const CUtensorMap* kv_map, i
     }
     dim3 grid(p.n_splits, p.hkv, n_dec_grid);
     attn_decode_kernel<D, G><<<grid, 128, smem, s>>>(p);
-    if (p.n_splits > 1) attn_decode_combine_kernel<D, G><<<dim3(n_dec_grid, p.hkv), 256, 0, s>>>(p, n_dec_grid);
   }
   if (n_pt_grid > 0) launch_prefill_tc(p, kv_map, D, G, n_pt_grid, s);
 }

@@ -42,7 +42,8 @@ void silu_mul(const __nv_bfloat16* gu, __nv_bfloat16* act, int ffn, const IterDe
 void rope_append(__nv_bfloat16* qkv, const int32_t* tok_pos, const int32_t* tok_slot, __nv_bfloat16* pool, int hq,
                  int hkv, int D, int num_layers, int layer, float theta, const IterDesc* desc, int grid,
                  cudaStream_t s);
-void argmax_rows(const float* logits, int vocab, int32_t* out, const IterDesc* desc, int grid, cudaStream_t s);
+void argmax_rows(const float* logits, int vocab, unsigned long long* keys, const IterDesc* desc, int grid,
+                 cudaStream_t s);
 void safepoint(IterDesc* desc, PreemptMailbox* mb, int layer, cudaStream_t s);
 void safepoint_vote(__nv_bfloat16* tail, const IterDesc* desc, const PreemptMailbox* mb, cudaStream_t s);
 void safepoint_agreed(IterDesc* desc, PreemptMailbox* mb, const __nv_bfloat16* tail, int layer, cudaStream_t s);
@@ -218,6 +219,7 @@ struct cs_engine {
   float* ws = nullptr;
   size_t ws_floats = 0;
   float* ws2 = nullptr;  // K2 split-K partials
+  int32_t* dec_cnt = nullptr;  // K1 split-K arrival counters
   size_t ws2_floats = 0;
   uint8_t* d_meta = nullptr;
   uint8_t* h_meta = nullptr;
@@ -461,7 +463,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
       }
     }
     n_launch += (l == 0 ? 1 : 0) + (is_sp(l) ? 1 : 0) + 4 + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
-                (it.n_dec > 0 ? (it.splits > 1 ? 2 : 1) : 0) + (it.n_pt > 0 ? (it.k2_splits > 1 ? 2 : 1) : 0);
+                (it.n_dec > 0 ? 1 : 0) + (it.n_pt > 0 ? (it.k2_splits > 1 ? 2 : 1) : 0);
     if (it.paced) CK(cudaEventRecord(ev_layer[l], s_compute));
     if ((cfg.flags & CS_FLAG_SYNC_DEBUG) && !graph) {
       CK(cudaStreamSynchronize(s_compute));
@@ -472,9 +474,11 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   const int E = Eg;
   csk::add_rmsnorm(x, tmp, w.final_norm, xl, hidden, cfg.rms_eps, desc, it.d_ent_last, E, s_compute);
   gemm(xl, w.lm_head, logits, E, vocab, hidden, true);
-  csk::argmax_rows(logits, vocab, reinterpret_cast<int32_t*>(d_out + sizeof(csk::IterDesc)), desc, E, s_compute);
+  csk::argmax_rows(logits, vocab, reinterpret_cast<unsigned long long*>(d_out + sizeof(csk::IterDesc)), desc, E,
+                   s_compute);
   CK(cudaMemcpyAsync(d_out, d_meta, sizeof(csk::IterDesc), cudaMemcpyDeviceToDevice, s_compute));
-  CK(cudaMemcpyAsync(h_out, d_out, sizeof(csk::IterDesc) + sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s_compute));
+  CK(cudaMemcpyAsync(h_out, d_out, sizeof(csk::IterDesc) + sizeof(uint64_t) * E, cudaMemcpyDeviceToHost,
+                     s_compute));
   n_launch += 2;
   return n_launch;
 }
@@ -747,6 +751,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     ap.dec_ent = reinterpret_cast<const int32_t*>(d + o_dec);
     ap.tiles = reinterpret_cast<const csk::PrefillTile*>(d + o_tiles);
     ap.ws = e->ws;
+    ap.dec_cnt = e->dec_cnt;
     ap.num_layers = e->L;
     ap.hq = e->hq;
     ap.hkv = e->hkv;
@@ -935,8 +940,10 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         CK(cudaMalloc(&e->act, T * e->ffn * 2));
         CK(cudaMalloc(&e->xl, e->max_ent * H * 2));
         CK(cudaMalloc(&e->logits, static_cast<size_t>(e->max_ent) * e->vocab * 4));
-        CK(cudaMalloc(&e->d_out, sizeof(csk::IterDesc) + 4 * e->max_ent));
-        CK(cudaMallocHost(&e->h_out, sizeof(csk::IterDesc) + 4 * e->max_ent));
+        CK(cudaMalloc(&e->d_out, sizeof(csk::IterDesc) + 8 * e->max_ent));
+        CK(cudaMalloc(&e->dec_cnt, sizeof(int32_t) * e->max_ent * e->hkv));
+        CK(cudaMemset(e->dec_cnt, 0, sizeof(int32_t) * e->max_ent * e->hkv));
+        CK(cudaMallocHost(&e->h_out, sizeof(csk::IterDesc) + 8 * e->max_ent));
         CKB(cublasCreate(&e->blas));
         CKB(cublasSetStream(e->blas, e->s_compute));
         CK(cudaMalloc(&e->blas_ws, 64u << 20));
@@ -1000,7 +1007,8 @@ int cs_destroy(cs_engine* e) {
       for (void* p : {static_cast<void*>(e->x), static_cast<void*>(e->xn), static_cast<void*>(e->qkv),
                       static_cast<void*>(e->attn), static_cast<void*>(e->tmp), static_cast<void*>(e->gu),
                       static_cast<void*>(e->act), static_cast<void*>(e->xl), static_cast<void*>(e->logits),
-                      static_cast<void*>(e->ws), static_cast<void*>(e->ws2), static_cast<void*>(e->d_meta),
+                      static_cast<void*>(e->ws), static_cast<void*>(e->ws2), static_cast<void*>(e->dec_cnt),
+                      static_cast<void*>(e->d_meta),
                       static_cast<void*>(e->d_out),
                       e->blas_ws})
         if (p) cudaFree(p);
@@ -1329,7 +1337,8 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
       CK(cudaEventElapsedTime(&ms, e->ev_start, e->ev_end));
       inf.gpu_ms = ms;
       const auto* desc = reinterpret_cast<const csk::IterDesc*>(e->h_out);
-      const int32_t* ids = reinterpret_cast<const int32_t*>(e->h_out + sizeof(csk::IterDesc));
+      // argmax keys: low 32 bits = ~id (0 -> -1 for rows past n_ent_cur)
+      const uint64_t* keys = reinterpret_cast<const uint64_t*>(e->h_out + sizeof(csk::IterDesc));
       if (desc->dropped_at >= 0) {
         inf.preempted_at_layer = desc->dropped_at;
         n_alive = it.n_ent_on;
@@ -1340,10 +1349,11 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
       }
       inf.n_outputs = n_alive;
       inf.h2d_bytes = it.meta_bytes;
-      inf.d2h_bytes = static_cast<int64_t>(sizeof(csk::IterDesc) + sizeof(int32_t) * it.n_ent);
+      inf.d2h_bytes = static_cast<int64_t>(sizeof(csk::IterDesc) + sizeof(uint64_t) * (it.graph ? it.bucket : it.n_ent));
       inf.gemm_trunc_layer = it.gemm_trunc_layer;
       if (out_tokens)
-        for (int i = 0; i < n_alive && i < cap; ++i) out_tokens[i] = ids[i];
+        for (int i = 0; i < n_alive && i < cap; ++i)
+          out_tokens[i] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(keys[i] & 0xFFFFFFFFull));
       if (logits && n_alive > 0)
         CK(cudaMemcpy(logits, e->logits, static_cast<size_t>(n_alive) * e->vocab * 4, cudaMemcpyDeviceToHost));
     } else {

@@ -1,6 +1,8 @@
 // Element-wise / row kernels of the layer forward, the KV
 // append (K3), the preemption safepoint (K6) and the checkpoint gather /
 // restore scatter over the host link (K4 / K5).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace csk {
@@ -51,6 +53,9 @@ void embed(__nv_bfloat16* x, const __nv_bfloat16* emb, const int32_t* tok_ids, i
 // x[r] += add[r] (if add), xn[r'] = x[r] * rsqrt(mean(x^2) + eps) * w.
 // rows: the row set is all token rows (< n_tok_cur) or, with row_idx, the
 // gathered rows row_idx[i] for i < n_ent_cur (final norm of sampled rows).
+// One CTA per row, CH 16-byte chunks per thread kept in registers: one read
+// of x (and add), one write of x and xn.
+template <int CH>
 __global__ void add_rmsnorm_kernel(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16* w,
                                    __nv_bfloat16* xn, int hidden, float eps, const IterDesc* desc,
                                    const int32_t* row_idx) {
@@ -65,32 +70,35 @@ __global__ void add_rmsnorm_kernel(__nv_bfloat16* x, const __nv_bfloat16* add, c
   }
   __nv_bfloat16* xr = x + static_cast<size_t>(r) * hidden;
   const __nv_bfloat16* ar = add ? add + static_cast<size_t>(r) * hidden : nullptr;
-  extern __shared__ float sbuf[];  // hidden floats + 32 partials
+  float v[CH][8];
   float ss = 0.f;
-  for (int c = threadIdx.x * 8; c < hidden; c += blockDim.x * 8) {
-    uint4 xv = *reinterpret_cast<const uint4*>(xr + c);
-    const __nv_bfloat16* xe = reinterpret_cast<const __nv_bfloat16*>(&xv);
-    float v[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(xe[j]);
+  for (int k = 0; k < CH; ++k) {
+    const int c = (k * blockDim.x + threadIdx.x) * 8;
+    if (c >= hidden) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[k][j] = 0.f;
+      continue;
+    }
+    const uint4 xv = *reinterpret_cast<const uint4*>(xr + c);
+    const __nv_bfloat16* xe = reinterpret_cast<const __nv_bfloat16*>(&xv);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[k][j] = __bfloat162float(xe[j]);
     if (ar) {
-      uint4 av = *reinterpret_cast<const uint4*>(ar + c);
+      const uint4 av = *reinterpret_cast<const uint4*>(ar + c);
       const __nv_bfloat16* ae = reinterpret_cast<const __nv_bfloat16*>(&av);
       __nv_bfloat16 outv[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        outv[j] = __float2bfloat16(v[j] + __bfloat162float(ae[j]));
-        v[j] = __bfloat162float(outv[j]);
+        outv[j] = __float2bfloat16(v[k][j] + __bfloat162float(ae[j]));
+        v[k][j] = __bfloat162float(outv[j]);
       }
-      *reinterpret_cast<uint4*>(xr + c) = *reinterpret_cast<uint4*>(outv);
+      *reinterpret_cast<uint4*>(xr + c) = *reinterpret_cast<const uint4*>(outv);
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      sbuf[c + j] = v[j];
-      ss += v[j] * v[j];
-    }
+    for (int j = 0; j < 8; ++j) ss += v[k][j] * v[k][j];
   }
-  float* part = sbuf + hidden;
+  __shared__ float part[32];
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
   __syncthreads();
@@ -102,21 +110,32 @@ __global__ void add_rmsnorm_kernel(__nv_bfloat16* x, const __nv_bfloat16* add, c
   __syncthreads();
   const float inv = rsqrtf(part[0] / hidden + eps);
   __nv_bfloat16* yr = xn + static_cast<size_t>(row_idx ? i : r) * hidden;
-  for (int c = threadIdx.x * 8; c < hidden; c += blockDim.x * 8) {
-    uint4 wv = *reinterpret_cast<const uint4*>(w + c);
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int c = (k * blockDim.x + threadIdx.x) * 8;
+    if (c >= hidden) continue;
+    const uint4 wv = *reinterpret_cast<const uint4*>(w + c);
     const __nv_bfloat16* we = reinterpret_cast<const __nv_bfloat16*>(&wv);
     __nv_bfloat16 outv[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) outv[j] = __float2bfloat16(sbuf[c + j] * inv * __bfloat162float(we[j]));
-    *reinterpret_cast<uint4*>(yr + c) = *reinterpret_cast<uint4*>(outv);
+    for (int j = 0; j < 8; ++j) outv[j] = __float2bfloat16(v[k][j] * inv * __bfloat162float(we[j]));
+    *reinterpret_cast<uint4*>(yr + c) = *reinterpret_cast<const uint4*>(outv);
   }
 }
 
 void add_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16* w, __nv_bfloat16* xn, int hidden,
                  float eps, const IterDesc* desc, const int32_t* row_idx, int grid, cudaStream_t s) {
   if (grid <= 0) return;
-  const int threads = hidden >= 2048 ? 256 : 64;
-  add_rmsnorm_kernel<<<grid, threads, (hidden + 32) * sizeof(float), s>>>(x, add, w, xn, hidden, eps, desc, row_idx);
+  const int vec = hidden / 8;
+  // <= 512 threads: CH = ceil(vec / 512) chunks each (hidden <= 16384)
+  const int threads = std::min(512, ((vec + 31) / 32) * 32);
+  const int ch = (vec + threads - 1) / threads;
+  if (ch == 1)
+    add_rmsnorm_kernel<1><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx);
+  else if (ch == 2)
+    add_rmsnorm_kernel<2><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx);
+  else
+    add_rmsnorm_kernel<4><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx);
 }
 
 // ----------------------------------------------------------------- SwiGLU ----
@@ -206,50 +225,40 @@ void rope_append(__nv_bfloat16* qkv, const int32_t* tok_pos, const int32_t* tok_
 }
 
 // ---------------------------------------------------------------- argmax ----
-__global__ void argmax_kernel(const float* logits, int vocab, int32_t* out, const IterDesc* desc) {
-  const int r = blockIdx.x;
-  if (r >= desc->n_ent_cur) {
-    if (threadIdx.x == 0) out[r] = -1;
-    return;
-  }
-  const float* row = logits + static_cast<size_t>(r) * vocab;
-  float best = -INFINITY;
-  int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
-    const float v = row[i];
-    if (v > best || (v == best && i < bi)) {
-      best = v;
-      bi = i;
-    }
-  }
-  __shared__ float sv[32];
-  __shared__ int si[32];
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > best || (ov == best && oi < bi)) {
-      best = ov;
-      bi = oi;
-    }
-  }
-  if ((threadIdx.x & 31) == 0) {
-    sv[threadIdx.x >> 5] = best;
-    si[threadIdx.x >> 5] = bi;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
-      if (sv[w] > best || (sv[w] == best && si[w] < bi)) {
-        best = sv[w];
-        bi = si[w];
-      }
-    }
-    out[r] = bi;
-  }
+// Greedy sample: argmax over the vocab per sampled row, ties -> lowest id.
+// 16 CTAs per row; each reduces its slice and folds (ordered value, ~id) into
+// one 64-bit key per row with atomicMax. keys must be zeroed first; a row
+// that stays 0 decodes to id -1 (rows >= n_ent_cur).
+__device__ __forceinline__ unsigned long long argmax_key(float v, int i) {
+  const uint32_t u = __float_as_uint(v);
+  const uint32_t o = (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // order-preserving
+  return (static_cast<unsigned long long>(o) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(i));
 }
 
-void argmax_rows(const float* logits, int vocab, int32_t* out, const IterDesc* desc, int grid, cudaStream_t s) {
-  if (grid > 0) argmax_kernel<<<grid, 256, 0, s>>>(logits, vocab, out, desc);
+__global__ void __launch_bounds__(256) argmax_kernel(const float* logits, int vocab, unsigned long long* keys,
+                                                     const IterDesc* desc) {
+  const int r = blockIdx.y;
+  if (r >= desc->n_ent_cur) return;
+  const float* row = logits + static_cast<size_t>(r) * vocab;
+  const int chunk = (vocab + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * chunk, i1 = min(vocab, i0 + chunk);
+  unsigned long long best = 0;
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const unsigned long long k = argmax_key(row[i], i);
+    best = k > best ? k : best;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long k = __shfl_xor_sync(0xffffffffu, best, o);
+    best = k > best ? k : best;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(&keys[r], best);
+}
+
+void argmax_rows(const float* logits, int vocab, unsigned long long* keys, const IterDesc* desc, int grid,
+                 cudaStream_t s) {
+  if (grid <= 0) return;
+  cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * grid, s);
+  argmax_kernel<<<dim3(16, grid), 256, 0, s>>>(logits, vocab, keys, desc);
 }
 
 // ------------------------------------------------------- safepoint (K6) ----

@@ -70,5 +70,25 @@ def gather(n_blocks=1024):
     eng.close()
 
 
+def step(n=32, ctx=4096, reps=3):
+    """A decode-only forward of the full Llama-3.1-8B (the CUDA-graph path):
+    n sequences at ctx tokens of context."""
+    cfg = cs.model_config("llama8b", gpu_kv_capacity=24 << 30, host_kv_capacity=1 << 30, max_batched_tokens=8192,
+                          instrumented=0, max_entries=256)
+    eng = cs.Engine(cfg)
+    for r in range(n):
+        eng.register_request(r, False)
+        assert eng.allocate(r, ctx).ok
+        eng.commit_allocations(r)
+    for rep in range(reps):
+        for r in range(n):
+            assert eng.allocate(r, 1).ok
+        info = eng.forward([cs.BatchEntry(r, 1, ctx + rep + 1, cs.CS_DECODE, False) for r in range(n)], epoch=rep + 1)
+        for r in range(n):
+            eng.commit_allocations(r)
+        print(f"step rep {rep}: {info.gpu_ms:.3f} ms", flush=True)
+    eng.close()
+
+
 if __name__ == "__main__":
-    {"decode": decode, "prefill": prefill, "gather": gather}[sys.argv[1]]()
+    {"decode": decode, "prefill": prefill, "gather": gather, "step": step}[sys.argv[1]]()
