@@ -55,8 +55,6 @@ void fill_pool(__nv_bfloat16* pool, size_t n, uint64_t seed, cudaStream_t s);
 bool launch_attention(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_dec_grid,
                       int n_pt_grid, cudaStream_t s);
 int prefill_tile_rows();
-bool gemm_skinny(const __nv_bfloat16* X, const __nv_bfloat16* W, void* Y, int M, int N, int K, bool out_f32,
-                 float* ws, size_t ws_floats, int32_t* cnt, int cnt_len, int sms, cudaStream_t s);
 }  // namespace csk
 
 namespace {
@@ -222,11 +220,6 @@ struct cs_engine {
   size_t ws_floats = 0;
   float* ws2 = nullptr;  // K2 split-K partials
   int32_t* dec_cnt = nullptr;  // K1 split-K arrival counters
-  float* sk_ws = nullptr;      // skinny-GEMM split-K partials
-  int32_t* sk_cnt = nullptr;   // skinny-GEMM arrival counters (self-resetting)
-  static constexpr size_t kSkWsFloats = 8u << 20;
-  static constexpr int kSkCnt = 4096;
-  int64_t own_gemms = 0;       // hand-written GEMM launches enqueued so far
   size_t ws2_floats = 0;
   uint8_t* d_meta = nullptr;
   uint8_t* h_meta = nullptr;
@@ -392,15 +385,6 @@ void make_kv_tensor_map(CUtensorMap* map, void* pool, uint64_t rows, int D) {
 // Row-major Y[M,N] = X[M,K] * W[N,K]^T on cuBLAS (plain library GEMM).
 void cs_engine::gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32) {
   if (M <= 0) return;
-  // few rows (decode steps): weight-streaming kernel at the HBM roofline;
-  // padded rows (up to 16) must exist in the buffers (activations hold
-  // max_tok rows, head buffers max_ent)
-  const int m_pad = (M + 15) / 16 * 16;
-  if (M <= 64 && m_pad <= (out_f32 ? max_ent : max_tok) &&
-      csk::gemm_skinny(A, W, C, M, N, K, out_f32, sk_ws, kSkWsFloats, sk_cnt, kSkCnt, sms, s_compute)) {
-    ++own_gemms;
-    return;
-  }
   const float alpha = 1.f, beta = 0.f;
   CKB(cublasGemmEx(blas, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, W, CUDA_R_16BF, K, A, CUDA_R_16BF, K, &beta, C,
                    out_f32 ? CUDA_R_32F : CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
@@ -422,7 +406,6 @@ int64_t cs_engine::layer_gemm_rows(int layer) {
 // plan's counts, or the graph bucket's); returns the kernels it launched.
 int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   int n_launch = 0;
-  const int64_t own0 = own_gemms;
   const auto* desc = reinterpret_cast<const csk::IterDesc*>(d_meta);
   auto* desc_mut = reinterpret_cast<csk::IterDesc*>(d_meta);
   const int lookahead = cfg.layer_lookahead > 0 ? cfg.layer_lookahead : 2;
@@ -497,7 +480,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   CK(cudaMemcpyAsync(h_out, d_out, sizeof(csk::IterDesc) + sizeof(uint64_t) * E, cudaMemcpyDeviceToHost,
                      s_compute));
   n_launch += 2;
-  return n_launch + static_cast<int>(own_gemms - own0);
+  return n_launch;
 }
 
 // Enqueues every layer of the current iteration (caller or worker thread).
@@ -959,9 +942,6 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         CK(cudaMalloc(&e->logits, static_cast<size_t>(e->max_ent) * e->vocab * 4));
         CK(cudaMalloc(&e->d_out, sizeof(csk::IterDesc) + 8 * e->max_ent));
         CK(cudaMalloc(&e->dec_cnt, sizeof(int32_t) * e->max_ent * e->hkv));
-        CK(cudaMalloc(&e->sk_ws, sizeof(float) * cs_engine::kSkWsFloats));
-        CK(cudaMalloc(&e->sk_cnt, sizeof(int32_t) * cs_engine::kSkCnt));
-        CK(cudaMemset(e->sk_cnt, 0, sizeof(int32_t) * cs_engine::kSkCnt));
         CK(cudaMemset(e->dec_cnt, 0, sizeof(int32_t) * e->max_ent * e->hkv));
         CK(cudaMallocHost(&e->h_out, sizeof(csk::IterDesc) + 8 * e->max_ent));
         CKB(cublasCreate(&e->blas));
@@ -1028,7 +1008,6 @@ int cs_destroy(cs_engine* e) {
                       static_cast<void*>(e->attn), static_cast<void*>(e->tmp), static_cast<void*>(e->gu),
                       static_cast<void*>(e->act), static_cast<void*>(e->xl), static_cast<void*>(e->logits),
                       static_cast<void*>(e->ws), static_cast<void*>(e->ws2), static_cast<void*>(e->dec_cnt),
-                      static_cast<void*>(e->sk_ws), static_cast<void*>(e->sk_cnt),
                       static_cast<void*>(e->d_meta),
                       static_cast<void*>(e->d_out),
                       e->blas_ws})
