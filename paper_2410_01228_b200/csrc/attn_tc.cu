@@ -3,29 +3,29 @@
 // oracle_latency, proj/src/perf_model.cpp:56-65).
 //
 // One CTA = two 128-row query tiles (256 packed (token, head-in-group) rows of
-// one entry) x one KV head. Keys stream in tiles of 64 (4 pages of 16 tokens)
-// through a 4-stage shared-memory ring fed by TMA straight from the
+// one entry) x one KV head. Keys stream in tiles of 128 (8 pages of 16
+// tokens) through a 2-stage shared-memory ring fed by TMA straight from the
 // block-table-indexed HBM pool (one 2D tensor map over the pool's [rows][D]
 // view; a page of one (layer, K|V, head) is 16 contiguous rows), so every K/V
 // byte loaded serves 256 query rows. Warp roles (320 threads):
-//   warp 8      TMA producer (one lane): K and V pages of key tile j -> stage j%4
-//   warp 9      MMA issuer (one lane): S_i(j) = Q_i K_j^T (SS, M=128 N=64 K=D)
-//               into TMEM buffer S_i[j%2] one key tile AHEAD of the softmax,
-//               and O_i += P_i(j) V_j (TS: P_i read from TMEM, V_j from smem
-//               MN-major; M=128 N=D K=64) into TMEM O_i
+//   warp 8      TMA producer (elected lane): K and V pages of key tile j -> stage j%2
+//   warp 9      MMA issuer (elected lane), ping-pong over the two query tiles:
+//               S_i(j) = Q_i K_j^T (SS, M=128 N=128 K=D: full rate, smem at
+//               128 B/clk) into TMEM S_i, and O_i += P_i(j) V_j (TS: P_i read
+//               from TMEM, V_j from smem MN-major; M=128 N=D K=128) into TMEM O_i
 //   warps 0-3   softmax/epilogue of query tile 0, warps 4-7 of tile 1; one
 //               thread per row == one TMEM lane: tcgen05.ld the S row, causal
 //               mask on absolute positions (recompute positions may be
 //               non-contiguous), online softmax with lazy rescale (O_i in TMEM
 //               is corrected only when the row max grows by > 2^8), P_i as
-//               packed bf16 written back over the S buffer's columns
-//               (tcgen05.st), final O_i / l to HBM.
-// Because S is double-buffered per query tile, the softmax of key tile j never
-// waits for the tensor core: S(j+1) is computed while P(j) is being made.
-// TMEM (512 cols): S_0 [0,64) [64,128)  S_1 [128,192) [192,256)
-//                  O_0 [256,256+D)  O_1 [384,384+D).
+//               packed bf16 written back over S_i's columns (tcgen05.st),
+//               final O_i / l to HBM.
+// While softmax i makes P_i(j), the tensor core runs the other tile's PV and
+// S, so MUFU/ALU time overlaps the UMMA time (tools/umma_bench.cu: SS N=64
+// runs at 2/3 rate, smem-bound; SS N>=128 and TS at the full 4096 MAC/clk).
+// TMEM (512 cols): S_0 [0,128)  S_1 [128,256)  O_0 [256,256+D)  O_1 [384,384+D).
 // mbarriers (each waited at most one phase behind): k_full/v_full/kv_empty
-// per stage, s_full/p_full per (query tile, S buffer), o_done per query tile.
+// per stage, s_full/p_full/o_done per query tile, o_final after the last PV.
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -62,12 +62,12 @@ namespace {
 
 constexpr int kRows = 128;   // UMMA M: rows per query tile
 constexpr int kQT = 2;       // query tiles per CTA
-constexpr int kKeys = 64;    // keys per tile (UMMA N of S, K of PV)
-constexpr int kStages = 4;   // K/V ring depth
+constexpr int kKeys = 128;   // keys per tile (UMMA N of S, K of PV)
+constexpr int kStages = 2;   // K/V ring depth
 constexpr int kPage = 16;
 constexpr int kThreads = 320;
 constexpr int kChunkBytes = 128 * 128;        // [128 rows][64 bf16] SWIZZLE_128B chunk (Q) = 16 KB
-constexpr int kKvChunkBytes = kKeys * 128;    // [64 keys][64 bf16] chunk (K, V) = 8 KB
+constexpr int kKvChunkBytes = kKeys * 128;    // [128 keys][64 bf16] chunk (K, V) = 16 KB
 
 template <int D>
 struct TcLayout {
@@ -79,7 +79,7 @@ struct TcLayout {
   static constexpr int bytes = bar + 256 + 1024;                     // barriers + 1 KB alignment slack
   // one CTA per SM (each allocates all 512 TMEM columns)
   static constexpr int launch_bytes = bytes < 120 * 1024 ? 120 * 1024 : bytes;
-  static constexpr int tmem_s = 0;      // + i * 128 + buffer * 64
+  static constexpr int tmem_s = 0;      // + i * 128
   static constexpr int tmem_o = 256;    // + i * 128
 };
 
@@ -134,9 +134,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* k_full = bars + 0;                   // [kStages]
   uint64_t* v_full = k_full + kStages;           // [kStages]
   uint64_t* kv_empty = v_full + kStages;         // [kStages]
-  uint64_t* s_full = kv_empty + kStages;         // [query tile][S buffer]
-  uint64_t* p_full = s_full + 4;                 // [query tile][S buffer]
-  uint64_t* o_done = p_full + 4;                 // [query tile] once per PV
+  uint64_t* s_full = kv_empty + kStages;         // [query tile]
+  uint64_t* p_full = s_full + 2;                 // [query tile]
+  uint64_t* o_done = p_full + 2;                 // [query tile] once per PV
   uint64_t* o_final = o_done + 2;                // [query tile] after the last PV
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 2);
 
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_init(&v_full[i], 1);
       tc::mbar_init(&kv_empty[i], 1);
     }
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&s_full[i], 1);
       tc::mbar_init(&p_full[i], kRows);
     }
@@ -187,13 +187,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------ TMA producer --
     // warp-wide loop, one elected lane issues
     {
-      constexpr uint32_t kTileBytes = CH * kKvChunkBytes;  // 64 keys x D bf16
+      constexpr uint32_t kTileBytes = CH * kKvChunkBytes;  // 128 keys x D bf16
       for (int j = 0; j < n_kt; ++j) {
         const int st = j % kStages;
         if (j >= kStages) K2_WAIT(&kv_empty[st], ((j / kStages) - 1) & 1, "kv_empty", j);
-        // lane pi < 4 resolves page pi of the tile (pages past the last one
+        // lane pi < 8 resolves page pi of the tile (pages past the last one
         // reload a valid page: masked to p = 0, finite V keeps 0 * V == 0)
-        const int pg = min((jb + j) * (kKeys / kPage) + (lane & 3), n_pages - 1);
+        const int pg = min((jb + j) * (kKeys / kPage) + (lane & 7), n_pages - 1);
         const int32_t blk = bt[pg];
         int32_t pblk[kKeys / kPage];
 #pragma unroll
@@ -224,11 +224,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_o = tc::idesc_bf16_f32(kRows, D, false, true);
       const uint32_t q_addr = tc::smem_u32(sQ), k_addr = tc::smem_u32(sK), v_addr = tc::smem_u32(sV);
       const int nq = has2 ? 2 : 1;
-      // S_i(j) -> buffer j%2; needs K_j landed
+      // S_i(j) -> TMEM S_i; needs K_j landed
       auto issue_s = [&](int qi, int j) {
         const uint32_t kb = k_addr + (j % kStages) * CH * kKvChunkBytes;
         const uint32_t qb = q_addr + qi * CH * kChunkBytes;
-        const uint32_t d_tmem = tmem + Lay::tmem_s + qi * 128 + (j & 1) * kKeys;
+        const uint32_t d_tmem = tmem + Lay::tmem_s + qi * 128;
         if (tc::elect_one_sync()) {
 #pragma unroll
           for (int ks = 0; ks < D / 16; ++ks) {
@@ -237,14 +237,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::umma_bf16_ss(d_tmem, tc::sdesc_sw128(qb + qoff, 16, 1024), tc::sdesc_sw128(kb + koff, 16, 1024),
                              idesc_s, ks > 0 ? 1u : 0u);
           }
-          tc::umma_commit(&s_full[qi * 2 + (j & 1)]);
+          tc::umma_commit(&s_full[qi]);
         }
         __syncwarp();
       };
-      // O_i += P_i(j) V_j; P_i(j) is packed bf16 in S buffer j%2
+      // O_i += P_i(j) V_j; P_i(j) is packed bf16 over S_i's first 64 columns
       auto issue_pv = [&](int qi, int j, bool release_stage) {
         const uint32_t vb = v_addr + (j % kStages) * CH * kKvChunkBytes;
-        const uint32_t pa = tmem + Lay::tmem_s + qi * 128 + (j & 1) * kKeys;
+        const uint32_t pa = tmem + Lay::tmem_s + qi * 128;
         const uint32_t d_tmem = tmem + Lay::tmem_o + qi * 128;
         if (tc::elect_one_sync()) {
 #pragma unroll
@@ -270,27 +270,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         K2T_ADD(t_wk, t0);
         tc::tc_fence_after();
       };
-      // prologue: S(0) and S(1) for both query tiles
-      for (int j = 0; j < min(2, n_kt); ++j) {
-        wait_k(j);
-        for (int qi = 0; qi < nq; ++qi) issue_s(qi, j);
-      }
+      // prologue: S(0) for both query tiles
+      wait_k(0);
+      for (int qi = 0; qi < nq; ++qi) issue_s(qi, 0);
+      // ping-pong: while softmax i makes P_i(j), the tensor core runs the
+      // other tile's PV / S
       for (int j = 0; j < n_kt; ++j) {
         const int st = j % kStages;
         long long t0 = K2T_NOW();
         K2_WAIT(&v_full[st], (j / kStages) & 1, "v_full", j);
         K2T_ADD(t_wv, t0);
-        const bool ahead = j + 2 < n_kt;
-        if (ahead) wait_k(j + 2);
+        const bool next = j + 1 < n_kt;
+        if (next) wait_k(j + 1);
         for (int qi = 0; qi < nq; ++qi) {
           t0 = K2T_NOW();
-          K2_WAIT(&p_full[qi * 2 + (j & 1)], (j >> 1) & 1, "p_full", j);
+          K2_WAIT(&p_full[qi], j & 1, "p_full", j);
           K2T_ADD(t_wp, t0);
           tc::tc_fence_after();
           issue_pv(qi, j, qi == nq - 1);
-          // S_i(j+2) reuses buffer j%2: issued after PV_i(j), its last reader
-          // (UMMAs from one thread execute in issue order)
-          if (ahead) issue_s(qi, j + 2);
+          // S_i(j+1) overwrites the P_i(j) columns PV_i(j) reads: UMMAs from
+          // one thread execute in issue order
+          if (next) issue_s(qi, j + 1);
         }
       }
 #ifdef CS_K2_TIMERS
@@ -316,10 +316,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       K2T_DECL(t_wo);
       const long long t_sbegin = K2T_NOW();
       for (int j = 0; j < n_kt; ++j) {
-        const int b = j & 1;
-        const uint32_t ts = ts0 + b * kKeys;
+        const uint32_t ts = ts0;
         const long long t0 = K2T_NOW();
-        K2_WAIT(&s_full[qi * 2 + b], (j >> 1) & 1, "s_full", j);
+        K2_WAIT(&s_full[qi], j & 1, "s_full", j);
         K2T_ADD(t_ws, t0);
         tc::tc_fence_after();
         float s[kKeys];
@@ -328,13 +327,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tmem_wait_ld();
         tc::reg_fence<kKeys>(s);
         const int kbase = (jb + j) * kKeys;
-        float mx = -INFINITY;  // raw (unscaled) max; scale > 0 commutes with max
         if (kbase + kKeys - 1 > pos) {  // diagonal tile: causal mask
 #pragma unroll
           for (int i = 0; i < kKeys; ++i) s[i] = (kbase + i <= pos) ? s[i] : -INFINITY;
         }
+        // raw (unscaled) max, 8 independent chains; scale > 0 commutes with max
+        float mxa[8];
 #pragma unroll
-        for (int i = 0; i < kKeys; ++i) mx = fmaxf(mx, s[i]);
+        for (int a = 0; a < 8; ++a) mxa[a] = s[a];
+#pragma unroll
+        for (int i = 8; i < kKeys; ++i) mxa[i & 7] = fmaxf(mxa[i & 7], s[i]);
+        const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                               fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
         const float m_new = fmaxf(m_used, mx * scale);
         const bool rescale = m_new > m_used + 8.f;  // true on the first tile (m_used = -inf)
         const float alpha = rescale ? tc::ex2_approx(m_used - m_new) : 1.f;
@@ -342,14 +346,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         // a split's rows may see no valid key yet (m_used = -inf): p = 0
         const float msub = m_used == -INFINITY ? 0.f : m_used;
         uint32_t pk[kKeys / 2];
-        float rs = 0.f;
+        float rsa[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < kKeys; i += 2) {
           const float p0 = tc::ex2_approx(fmaf(s[i], scale, -msub));
           const float p1 = tc::ex2_approx(fmaf(s[i + 1], scale, -msub));
-          rs += p0 + p1;
+          rsa[(i >> 1) & 3] += p0 + p1;
           pk[i / 2] = pack_bf16(p0, p1);
         }
+        const float rs = (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
         l = l * alpha + rs;
         // tcgen05.ld/st are warp-collective (.sync.aligned): the correction
         // runs for the whole warp if any of its rows needs it (alpha = 1 for
@@ -370,12 +375,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::tmem_st32(to + c * 32, o);
           }
         }
-        // P_i(j) over the S buffer's first 32 columns (S_i(j) is in registers;
-        // PV_i(j-2), the previous reader of this buffer, ran before S_i(j))
+        // P_i(j) over S_i's first 64 columns (S_i(j) is in registers; PV_i(j-1),
+        // the previous reader, ran before S_i(j))
         tc::tmem_st32u(ts, pk);
+        tc::tmem_st32u(ts + 32, pk + 32);
         tc::tmem_wait_st();
         tc::tc_fence_before();
-        tc::mbar_arrive(&p_full[qi * 2 + b]);
+        tc::mbar_arrive(&p_full[qi]);
       }
 #ifdef CS_K2_TIMERS
       if (r == 0 && blockIdx.y == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && blockIdx.z == 0)
