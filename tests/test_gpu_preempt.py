@@ -51,3 +51,28 @@ def test_online_only_plan_is_never_dropped():
     info, lg, ref = drv.step([(0, None)], preempt_after_launch=True)
     assert info.preempted_at_layer is None
     drv.close()
+
+
+def test_decode_only_graph_iteration_drops_offline():
+    """Decode-only plans run as a captured CUDA graph (with the safepoint
+    kernels inside): a flag for this epoch still drops the offline decodes at
+    a layer boundary, online outputs match the oracle, and a later decode-only
+    step of the same bucket (graph replay) is unaffected."""
+    drv = Driver(_cfg())
+    drv.add(0, 40, online=True)
+    drv.add(1, 50, online=False)
+    drv.add(2, 60, online=False)
+    drv.step([(0, None), (1, None), (2, None)])      # prefills (not a graph)
+    # decode-only step, preempted right after launch
+    info, lg, ref = drv.step([(0, None), (1, None), (2, None)], preempt_after_launch=True)
+    if info.preempted_at_layer is not None:            # the flag may land after the last safepoint
+        assert info.n_outputs == 1
+        assert drv.known[1] == 51 and drv.known[2] == 61  # offline decodes rolled back
+    assert float(np.max(np.abs(lg[:1] - ref[:1]))) <= 2e-2
+    # unpreempted decode-only steps replay the same bucket's graph
+    for _ in range(2):
+        info, lg, ref = drv.step([(0, None), (1, None), (2, None)])
+        assert info.preempted_at_layer is None
+        assert float(np.max(np.abs(lg - ref))) <= 2e-2
+    drv.eng.audit()
+    drv.close()
