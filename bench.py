@@ -331,6 +331,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-probes", action="store_true")
     ap.add_argument("--dump", default=None, help="write per-iteration device times + plan shapes (.npz)")
+    ap.add_argument("--workload", default="llama8b", choices=["llama8b", "llama70b"],
+                    help="llama8b: BASELINE config 2 (default, the headline); llama70b: config 4's model and "
+                         "online spike on ONE B200 (tests/golden/llama70b_b200)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -361,7 +364,8 @@ def main():
         K = args.steps if args.steps > 0 else tr.n_iter - W
         K = min(K, tr.n_iter - W)
         # replicas: every rank replays the whole trace on its own GPU (weak scaling)
-        cfg = R.engine_config_for(tr, "llama8b", device=local, max_entries=256)
+        cfg = R.engine_config_for(tr, "llama70b" if name.startswith("llama70b") else "llama8b", device=local,
+                                  max_entries=256)
         t_setup = time.time()
         eng = cs.Engine(cfg)
         setup_s = time.time() - t_setup
@@ -393,9 +397,11 @@ def main():
     # headline: the reference scheduler planning on B200-measured latencies
     # (profile -> fit closed loop); the H100-calibrated schedule beside it
     main_trace = "llama8b_b200" if os.path.isdir(os.path.join(ROOT, "tests", "golden", "llama8b_b200")) else "llama8b"
+    if args.workload == "llama70b":
+        main_trace = "llama70b_b200"
     rp = replay(main_trace)
     other = None
-    if main_trace != "llama8b" and not args.no_probes:
+    if main_trace == "llama8b_b200" and not args.no_probes:
         o = replay("llama8b")
         other = {"workload": "llama8b (reference 8B preset oracle: H100-calibrated schedule)",
                  "value": world * o["off"] / o["gpu_s"], "e2e": world * o["off"] / o["wall_s"],
@@ -448,11 +454,16 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": int(res.iterations), "warmup": W,
         "ms_per_step": 1e3 * gpu_s / max(res.iterations, 1), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"{main_trace}: Llama-3.1-8B shape bf16, 1 B200 per rank, the reference's ConServe "
-                               "co-serving run (bursty online Gamma rate 3/s cv 2, 4096/256, 30 s + 64-request "
-                               "offline backlog with replenish, chunked prefill, 24 GiB KV pool, safepoint every "
-                               "layer)" + (", scheduled with the reference's own fit of the B200-measured latency "
-                                           "grid (profiles/b200_fit.json)" if main_trace.endswith("b200") else ""),
+        "config": {"workload": (f"{main_trace}: Llama-3.1-8B shape bf16, 1 B200 per rank, the reference's ConServe "
+                                "co-serving run (bursty online Gamma rate 3/s cv 2, 4096/256, 30 s + 64-request "
+                                "offline backlog with replenish, chunked prefill, 24 GiB KV pool, safepoint every "
+                                "layer)" + (", scheduled with the reference's own fit of the B200-measured latency "
+                                            "grid (profiles/b200_fit.json)" if main_trace.endswith("b200") else ""))
+                   if not main_trace.startswith("llama70b") else
+                   (f"{main_trace}: Llama-3.1-70B shape bf16 (80 layers, 141 GB of weights) on ONE B200, online "
+                    "spike 0.5 -> 2 req/s at 20 s (2048/128) against a 48-request offline backlog, 20 GiB KV pool, "
+                    "safepoint every layer, scheduled with the reference's fit of the B200 70B profile "
+                    "(profiles/b200_fit_70b.json)"),
                    "iterations": f"[{W}, {W + K}) of {tr.n_iter}", "parallelism": "replica" if n > 1 else "single",
                    "l2": "inputs larger than L2 (16 GB of weights + KV per step)"},
         "e2e": {"value": e2e, "unit": UNIT,

@@ -84,6 +84,36 @@ def scenario(name: str):
         # the scheduler budgets TBT x (1 - margin) (config.hpp:17-28)
         cfg["slo"]["safety_margin"] = 0.2
         return cfg, None
+    if name == "llama70b_b200":
+        # BASELINE config 4 on ONE B200 (141 GB of bf16 weights + a 20 GiB KV
+        # pool fit in 179 GiB): Llama-3.1-70B shape (80 layers, 327680 B/token),
+        # safepoint every layer, an online load spike (0.5 -> 2 req/s at 20 s,
+        # frozen as a trace) against a 48-request offline backlog, scheduled by
+        # the reference on the reference-fitted B200 70B profile
+        # (profiles/b200_fit_70b.json); host link at the measured pinned peaks.
+        import numpy as np
+        fit = json.load(open(os.path.join(ROOT, "profiles", "b200_fit_70b.json")))["coeffs"]
+        rng = np.random.default_rng(70)
+        trace = [{"t": 0.0, "class": "offline", "in": 2048, "out": 128} for _ in range(48)]
+        t = 0.0
+        while True:
+            t += float(rng.exponential(1.0 / (0.5 if t < 20.0 else 2.0)))
+            if t >= 40.0:
+                break
+            trace.append({"t": round(t, 6), "class": "online", "in": 2048, "out": 128})
+        cfg = {
+            "cluster": {"num_layers": 80, "safepoint_interval_layers": 1, "kv_bytes_per_token": 327680,
+                        "gpu_kv_capacity": 20 << 30, "host_kv_capacity": 64 << 30,
+                        "d2h_bandwidth": 57.1e9, "h2d_bandwidth": 55.6e9,
+                        "safepoint_check_cost_us": 5.0, "max_batched_tokens": 8192},
+            "oracle": {"k1": fit["a_lin"], "k2": fit["a_quad"], "k3": 0.0, "k4": fit["a_mem"],
+                       "k5": fit["a_const"], "noise_cv": 0.0},
+            "policy": {"kind": "conserve"},
+            "slo": {"ttft_slo_s": 0.6, "tbt_slo_s": 0.3, "safety_margin": 0.2},
+            "workload": {"trace": "TRACE"},
+            "seed": 1,
+        }
+        return cfg, trace
     if name.startswith("config1_"):
         # the config-1 trace under the other policies / ablations
         # (policy kinds: config.cpp:38-44; ablation switches: config.hpp:76-82)

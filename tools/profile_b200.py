@@ -33,9 +33,13 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--p-values", type=int, nargs="*", default=list(P_VALUES))
     ap.add_argument("--c-values", type=int, nargs="*", default=list(C_VALUES))
+    ap.add_argument("--preset", default="llama8b")
     args = ap.parse_args()
-    cfg = cs.model_config("llama8b", gpu_kv_capacity=12 << 30, host_kv_capacity=1 << 30, max_batched_tokens=8192,
-                          instrumented=0, max_entries=64)
+    kv_gib = 12 if args.preset == "llama8b" else 24
+    # forwards here are synchronous, so freed blocks need no quarantine
+    cfg = cs.model_config(args.preset, gpu_kv_capacity=kv_gib << 30, host_kv_capacity=1 << 30,
+                          max_batched_tokens=8192, instrumented=0, max_entries=64,
+                          flags=cs._ffi.CS_FLAG_NO_FWD_QUARANTINE)
     eng = cs.Engine(cfg)
     grid = []
     rid = 0
@@ -76,7 +80,7 @@ def main():
     finally:
         eng.close()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
-    json.dump({"grid": grid, "model": "llama8b bf16, 1 B200", "timing": "CUDA events, median of %d" % args.reps},
+    json.dump({"grid": grid, "model": f"{args.preset} bf16, 1 B200", "timing": "CUDA events, median of %d" % args.reps},
               open(args.out, "w"), indent=1)
 
 
