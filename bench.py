@@ -331,7 +331,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-probes", action="store_true")
     ap.add_argument("--dump", default=None, help="write per-iteration device times + plan shapes (.npz)")
-    ap.add_argument("--workload", default="llama8b", choices=["llama8b", "llama70b"],
+    ap.add_argument("--workload", default="llama8b", choices=["llama8b", "qwen14b", "llama70b"],
                     help="llama8b: BASELINE config 2 (default, the headline); llama70b: config 4's model and "
                          "online spike on ONE B200 (tests/golden/llama70b_b200)")
     args = ap.parse_args()
@@ -364,8 +364,8 @@ def main():
         K = args.steps if args.steps > 0 else tr.n_iter - W
         K = min(K, tr.n_iter - W)
         # replicas: every rank replays the whole trace on its own GPU (weak scaling)
-        cfg = R.engine_config_for(tr, "llama70b" if name.startswith("llama70b") else "llama8b", device=local,
-                                  max_entries=256)
+        preset = "llama70b" if name.startswith("llama70b") else "qwen14b" if name.startswith("qwen14b") else "llama8b"
+        cfg = R.engine_config_for(tr, preset, device=local, max_entries=256)
         t_setup = time.time()
         eng = cs.Engine(cfg)
         setup_s = time.time() - t_setup
@@ -397,8 +397,8 @@ def main():
     # headline: the reference scheduler planning on B200-measured latencies
     # (profile -> fit closed loop); the H100-calibrated schedule beside it
     main_trace = "llama8b_b200" if os.path.isdir(os.path.join(ROOT, "tests", "golden", "llama8b_b200")) else "llama8b"
-    if args.workload == "llama70b":
-        main_trace = "llama70b_b200"
+    if args.workload != "llama8b":
+        main_trace = f"{args.workload}_b200"
     rp = replay(main_trace)
     other = None
     if main_trace == "llama8b_b200" and not args.no_probes:
@@ -459,7 +459,11 @@ def main():
                                 "offline backlog with replenish, chunked prefill, 24 GiB KV pool, safepoint every "
                                 "layer)" + (", scheduled with the reference's own fit of the B200-measured latency "
                                             "grid (profiles/b200_fit.json)" if main_trace.endswith("b200") else ""))
-                   if not main_trace.startswith("llama70b") else
+                   if main_trace.startswith("llama8b") else
+                   (f"{main_trace}: Qwen-2.5-14B shape bf16 (48 layers, 40/8 heads) on ONE B200, bursty online "
+                    "2 req/s cv 2 (4096/256, 30 s) + 64-request offline backlog, 40 GiB KV pool, TBT SLO 200 ms, "
+                    "scheduled with the reference's fit of the B200 14B profile (profiles/b200_fit_14b.json)")
+                   if main_trace.startswith("qwen14b") else
                    (f"{main_trace}: Llama-3.1-70B shape bf16 (80 layers, 141 GB of weights) on ONE B200, online "
                     "spike 0.5 -> 2 req/s at 20 s (2048/128) against a 48-request offline backlog, 20 GiB KV pool, "
                     "safepoint every layer, scheduled with the reference's fit of the B200 70B profile "

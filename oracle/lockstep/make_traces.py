@@ -84,6 +84,26 @@ def scenario(name: str):
         # the scheduler budgets TBT x (1 - margin) (config.hpp:17-28)
         cfg["slo"]["safety_margin"] = 0.2
         return cfg, None
+    if name == "qwen14b_b200":
+        # BASELINE config 3's model (Qwen-2.5-14B shape: 48 layers, 40/8 heads,
+        # 196608 B/token -- the reference presets' own KV unit) on ONE B200,
+        # the llama8b workload at 2 req/s online, a 40 GiB KV pool, scheduled
+        # on the reference-fitted B200 14B profile (profiles/b200_fit_14b.json)
+        cfg, _ = scenario("llama8b")
+        fit = json.load(open(os.path.join(ROOT, "profiles", "b200_fit_14b.json")))["coeffs"]
+        cfg["cluster"]["num_layers"] = 48
+        cfg["cluster"]["kv_bytes_per_token"] = 196608
+        cfg["cluster"]["gpu_kv_capacity"] = 40 << 30
+        # 3 req/s of 4096/256 online work exceeds a 14B on one GPU: the
+        # reference scheduler then stops dispatching ("event queue drained")
+        cfg["workload"]["online"]["rate"] = 2.0
+        cfg["oracle"] = {"k1": fit["a_lin"], "k2": fit["a_quad"], "k3": 0.0, "k4": fit["a_mem"],
+                         "k5": fit["a_const"], "noise_cv": 0.0}
+        # the 14B single-entry fit prices a decode at ~1 ms of KV traffic at 4K
+        # context; 90 online decodes then exceed a 100 ms budget and the
+        # reference scheduler drains its queue -> a 200 ms TBT SLO
+        cfg["slo"] = {"ttft_slo_s": 1.0, "tbt_slo_s": 0.2, "safety_margin": 0.2}
+        return cfg, None
     if name == "llama70b_b200":
         # BASELINE config 4 on ONE B200 (141 GB of bf16 weights + a 20 GiB KV
         # pool fit in 179 GiB): Llama-3.1-70B shape (80 layers, 327680 B/token),

@@ -27,7 +27,7 @@ from paper_2410_01228_b200 import replay as R
 from conftest import ROOT
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-PRESET = {"config1": "tiny", "llama8b": "llama8b", "llama70b": "llama70b", "fuzz": "qwen14b"}
+PRESET = {"config1": "tiny", "llama8b": "llama8b", "llama70b": "llama70b", "qwen14b": "qwen14b", "fuzz": "qwen14b"}
 SCENARIOS = sorted(d for d in os.listdir(GOLDEN) if os.path.exists(os.path.join(GOLDEN, d, "calls.jsonl.gz")))
 
 
