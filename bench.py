@@ -225,9 +225,37 @@ def preempt_latency_probe(cs, F, trials=20):
     finally:
         eng.close()
     lm = float(np.median(layer_ms)) * 1e3 if layer_ms else None
+    # no-preemption overhead of the safepoints (SPEC.md acceptance #6): the
+    # same unpreempted plan with safepoints every layer (+ host pacing) vs none
+    overhead = None
+    try:
+        plain = []
+        for instrumented in (0, 1):
+            c2 = cs.model_config("llama8b", gpu_kv_capacity=8 << 30, host_kv_capacity=1 << 30,
+                                 max_batched_tokens=8192, safepoint_interval_layers=1, instrumented=instrumented,
+                                 max_entries=256)
+            e2 = cs.Engine(c2)
+            try:
+                e2.register_request(0, True)
+                e2.register_request(1, False)
+                assert e2.allocate(0, 2049).ok
+                e2.commit_allocations(0)
+                times = []
+                for t in range(6):
+                    assert e2.allocate(1, 2048).ok
+                    plan = [cs.BatchEntry(0, 1, 2049, F.CS_DECODE, True),
+                            cs.BatchEntry(1, 2048, 0, F.CS_PREFILL, False)]
+                    times.append(e2.forward(plan, epoch=20_000 + t).gpu_ms)
+                    e2.rollback_allocations(1)
+                plain.append(float(np.median(times[2:])))
+            finally:
+                e2.close()
+        overhead = {"ms_without": plain[0], "ms_with": plain[1], "frac": plain[1] / plain[0] - 1.0}
+    except Exception as ex:  # never hide the main numbers
+        overhead = {"error": str(ex)}
     return {"trials": len(lat), "p50_us": percentile(lat, 0.5), "max_us": max(lat) if lat else None,
             "layer_time_us": lm, "under_one_layer": bool(lat) and lm is not None and max(lat) < lm,
-            "drop_layers": drop_layers[:8]}
+            "drop_layers": drop_layers[:8], "safepoint_overhead": overhead}
 
 
 def cpu_port_sample(tr, R, it_index):

@@ -7,6 +7,7 @@
 // `layer_lookahead` layers ahead of the device so the host can shrink the
 // GEMM M dimension once a preemption flag is seen, while the device-side
 // safepoint kernel truncates every other kernel at the layer boundary itself.
+#include <cublasLt.h>
 #include <cublas_v2.h>
 #include <cuda.h>
 #include <nccl.h>
@@ -236,6 +237,19 @@ struct cs_engine {
   bool any_forward = false;
   cublasHandle_t blas = nullptr;
   void* blas_ws = nullptr;
+  // cuBLASLt plans autotuned per decode-graph bucket (few-row GEMMs are
+  // latency/bandwidth bound and the default heuristic is not always the
+  // fastest there); key = M | N << 12 | K << 32 | f32 << 63
+  struct LtPlan {
+    cublasLtMatmulDesc_t op = nullptr;
+    cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
+    cublasLtMatmulAlgo_t algo{};
+  };
+  cublasLtHandle_t lt = nullptr;
+  std::map<uint64_t, LtPlan> lt_plans;
+  std::map<int, bool> lt_tuned;
+  void tune_gemms(int M);
+  bool lt_gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
   ncclComm_t comm = nullptr;
   DescRing ring[2];
   double moved_ms[2] = {0, 0};
@@ -383,8 +397,105 @@ void make_kv_tensor_map(CUtensorMap* map, void* pool, uint64_t rows, int D) {
 
 // ------------------------------------------------------------------ GEMM ----
 // Row-major Y[M,N] = X[M,K] * W[N,K]^T on cuBLAS (plain library GEMM).
+static uint64_t lt_key(int M, int N, int K, bool f32) {
+  return static_cast<uint64_t>(M) | (static_cast<uint64_t>(N) << 12) | (static_cast<uint64_t>(K) << 32) |
+         (static_cast<uint64_t>(f32) << 63);
+}
+
+bool cs_engine::lt_gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K,
+                        bool out_f32) {
+  auto f = lt_plans.find(lt_key(M, N, K, out_f32));
+  if (f == lt_plans.end()) return false;
+  const float alpha = 1.f, beta = 0.f;
+  const LtPlan& pl = f->second;
+  CKB(cublasLtMatmul(lt, pl.op, &alpha, W, pl.a, A, pl.b, &beta, C, pl.c, C, pl.c, &pl.algo, blas_ws, 64u << 20,
+                     s_compute));
+  return true;
+}
+
+// Times every heuristic candidate (up to 16) of the step's GEMM shapes at M
+// rows on the live weights and activation buffers (outputs land in buffers
+// the coming forward overwrites) and keeps the fastest; once per bucket,
+// before its graph is captured.
+void cs_engine::tune_gemms(int M) {
+  if (lt_tuned[M]) return;
+  lt_tuned[M] = true;
+  if (!lt) CKB(cublasLtCreate(&lt));
+  struct Shape {
+    const __nv_bfloat16 *A, *W;
+    void* C;
+    int N, K;
+    bool f32;
+  };
+  const int qkv_cols = (hq + 2 * hkv) * D;
+  const Shape shapes[] = {{xn, w.wqkv[0], qkv, qkv_cols, hidden, false},
+                          {attn, w.wo[0], tmp, hidden, hq * D, false},
+                          {xn, w.wgu[0], gu, 2 * ffn, hidden, false},
+                          {act, w.wd[0], tmp, hidden, ffn, false},
+                          {xl, w.lm_head, logits, vocab, hidden, true}};
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  for (const Shape& sh : shapes) {
+    if (sh.f32 && M > max_ent) continue;
+    LtPlan pl;
+    CKB(cublasLtMatmulDescCreate(&pl.op, CUBLAS_COMPUTE_32F, CUDA_R_32F));
+    const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
+    CKB(cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta)));
+    CKB(cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb)));
+    // column-major view: C[N, M] = W^T[N, K] * X^T[K, M]
+    CKB(cublasLtMatrixLayoutCreate(&pl.a, CUDA_R_16BF, sh.K, sh.N, sh.K));
+    CKB(cublasLtMatrixLayoutCreate(&pl.b, CUDA_R_16BF, sh.K, M, sh.K));
+    CKB(cublasLtMatrixLayoutCreate(&pl.c, sh.f32 ? CUDA_R_32F : CUDA_R_16BF, sh.N, M, sh.N));
+    cublasLtMatmulPreference_t pref;
+    CKB(cublasLtMatmulPreferenceCreate(&pref));
+    const size_t wsz = 64u << 20;
+    CKB(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsz, sizeof(wsz)));
+    cublasLtMatmulHeuristicResult_t res[16];
+    int n = 0;
+    const cublasStatus_t hs = cublasLtMatmulAlgoGetHeuristic(lt, pl.op, pl.a, pl.b, pl.c, pl.c, pref, 16, res, &n);
+    cublasLtMatmulPreferenceDestroy(pref);
+    float best = 1e30f;
+    int bi = -1;
+    const float alpha = 1.f, beta = 0.f;
+    for (int i = 0; hs == CUBLAS_STATUS_SUCCESS && i < n; ++i) {
+      if (res[i].state != CUBLAS_STATUS_SUCCESS) continue;
+      bool ok = true;
+      for (int rep = 0; rep < 2 && ok; ++rep)  // warm-up
+        ok = cublasLtMatmul(lt, pl.op, &alpha, sh.W, pl.a, sh.A, pl.b, &beta, sh.C, pl.c, sh.C, pl.c, &res[i].algo,
+                            blas_ws, wsz, s_compute) == CUBLAS_STATUS_SUCCESS;
+      if (!ok) continue;
+      CK(cudaEventRecord(e0, s_compute));
+      for (int rep = 0; rep < 5; ++rep)
+        cublasLtMatmul(lt, pl.op, &alpha, sh.W, pl.a, sh.A, pl.b, &beta, sh.C, pl.c, sh.C, pl.c, &res[i].algo,
+                       blas_ws, wsz, s_compute);
+      CK(cudaEventRecord(e1, s_compute));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (ms < best) {
+        best = ms;
+        bi = i;
+      }
+    }
+    if (bi >= 0) {
+      pl.algo = res[bi].algo;
+      lt_plans[lt_key(M, sh.N, sh.K, sh.f32)] = pl;
+    } else {
+      cublasLtMatmulDescDestroy(pl.op);
+      cublasLtMatrixLayoutDestroy(pl.a);
+      cublasLtMatrixLayoutDestroy(pl.b);
+      cublasLtMatrixLayoutDestroy(pl.c);
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CK(cudaGetLastError());
+}
+
 void cs_engine::gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32) {
   if (M <= 0) return;
+  if (lt_gemm(A, W, C, M, N, K, out_f32)) return;
   const float alpha = 1.f, beta = 0.f;
   CKB(cublasGemmEx(blas, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, W, CUDA_R_16BF, K, A, CUDA_R_16BF, K, &beta, C,
                    out_f32 ? CUDA_R_32F : CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
@@ -494,6 +605,11 @@ void cs_engine::enqueue_layers() {
     const uint64_t key = static_cast<uint64_t>(it.bucket) | (static_cast<uint64_t>(sp) << 16) | (graph_gen << 20);
     auto f = graphs.find(key);
     if (f == graphs.end()) {
+      static const bool no_tune = [] {
+        const char* v = std::getenv("CS_NO_GEMM_TUNE");
+        return v && v[0] == '1';
+      }();
+      if (!no_tune) tune_gemms(it.bucket);  // outside the capture: it times candidates
       GraphExec ge;
       cudaGraph_t g = nullptr;
       CK(cudaStreamBeginCapture(s_compute, cudaStreamCaptureModeThreadLocal));
@@ -998,6 +1114,13 @@ int cs_destroy(cs_engine* e) {
       e->mover.reset();
       for (auto& r : e->ring) r.live.clear();
       if (e->blas) cublasDestroy(e->blas);
+      for (auto& kv : e->lt_plans) {
+        cublasLtMatmulDescDestroy(kv.second.op);
+        cublasLtMatrixLayoutDestroy(kv.second.a);
+        cublasLtMatrixLayoutDestroy(kv.second.b);
+        cublasLtMatrixLayoutDestroy(kv.second.c);
+      }
+      if (e->lt) cublasLtDestroy(e->lt);
       if (e->comm) ncclCommDestroy(e->comm);
       cudaFree(e->kv);
       cudaFreeHost(e->host_kv);

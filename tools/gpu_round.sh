@@ -6,19 +6,20 @@
 #   parts: comma list of probe,tests,bench,launches,k1,k2,k4 (default all)
 set -u
 TAG=${1:-r1}
-PARTS=${2:-probe,tests,bench,launches,k1,k2,k4}
+PARTS=${2:-probe,smoke,tests,bench,launches,k1,k2,k4}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 has() { [[ ",$PARTS," == *",$1,"* ]]; }
 nproc > "$OUT/nproc.txt"
 nvidia-smi -q -d CLOCK > "$OUT/clocks_start.txt" 2>&1
 if has probe; then timeout 300 python tools/probe_box.py > "$OUT/probe.log" 2>&1; cp gpurun_out/probe_box.json "$OUT/" 2>/dev/null; fi
+if has smoke; then timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1; echo "smoke rc=$?" >> "$OUT/smoke.log"; fi
 if has tests; then timeout 900 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_gpu.log"; fi
 if has bench; then timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/bench.err"; fi
 NCU="ncu --clock-control none"
 if has launches; then
-  CS_NO_PACING=1 timeout 900 $NCU --metrics gpu__time_duration.sum -c 20000 --csv --log-file "$OUT/launches.csv" \
-    python bench.py --steps 60 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
+  CS_NO_PACING=1 timeout 1200 $NCU --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
+    python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
 fi
 if has k1; then
   timeout 600 $NCU --set full --import-source on -k regex:attn_decode_kernel -s 1 -c 1 -o "$OUT/k1_decode" -f \
