@@ -332,7 +332,7 @@ def pick_cpu_iteration(tr):
 
 def run_reference(args):
     from paper_2410_01228_b200 import replay as R
-    name = "llama8b_b200" if os.path.isdir(os.path.join(ROOT, "tests", "golden", "llama8b_b200")) else "llama8b"
+    name = "llama8b_b200_kv60"
     g = os.path.join(ROOT, "tests", "golden", name)
     tr = R.load(os.path.join(g, "calls.jsonl.gz"), os.path.join(g, "requests.jsonl.gz"))
     k = pick_cpu_iteration(tr)
@@ -359,6 +359,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-probes", action="store_true")
     ap.add_argument("--dump", default=None, help="write per-iteration device times + plan shapes (.npz)")
+    ap.add_argument("--h100", action="store_true", help="also replay the H100-calibrated (reference preset) schedule")
     ap.add_argument("--workload", default="llama8b", choices=["llama8b", "qwen14b", "llama70b"],
                     help="llama8b: BASELINE config 2 (default, the headline); llama70b: config 4's model and "
                          "online spike on ONE B200 (tests/golden/llama70b_b200)")
@@ -424,17 +425,26 @@ def main():
 
     # headline: the reference scheduler planning on B200-measured latencies
     # (profile -> fit closed loop); the H100-calibrated schedule beside it
-    main_trace = "llama8b_b200" if os.path.isdir(os.path.join(ROOT, "tests", "golden", "llama8b_b200")) else "llama8b"
-    if args.workload != "llama8b":
-        main_trace = f"{args.workload}_b200"
+    main_trace = "llama8b_b200_kv60" if args.workload == "llama8b" else f"{args.workload}_b200"
     rp = replay(main_trace)
-    other = None
-    if main_trace == "llama8b_b200" and not args.no_probes:
-        o = replay("llama8b")
-        other = {"workload": "llama8b (reference 8B preset oracle: H100-calibrated schedule)",
-                 "value": world * o["off"] / o["gpu_s"], "e2e": world * o["off"] / o["wall_s"],
-                 "online_p99_tpot_ms": percentile(o["tpot"], 0.99), "online_p99_tbt_ms": percentile(o["tbt"], 0.99),
-                 "offline_tokens": o["off"], "steps": int(o["res"].iterations)}
+
+    def summary(name, what):
+        o = replay(name)
+        so, s1o = o["s0"], o["s1"]
+        return {"workload": what, "value": world * o["off"] / o["gpu_s"], "e2e": world * o["off"] / o["wall_s"],
+                "online_p99_tpot_ms": percentile(o["tpot"], 0.99), "online_p99_tbt_ms": percentile(o["tbt"], 0.99),
+                "offline_tokens": o["off"], "steps": int(o["res"].iterations),
+                "d2h_bytes": s1o.moved_d2h_bytes - so.moved_d2h_bytes,
+                "h2d_bytes": s1o.moved_h2d_bytes - so.moved_h2d_bytes,
+                "replay_drops": int((o["res"].dropped_layer >= 0).sum())}
+
+    other, h100 = None, None
+    if args.workload == "llama8b" and not args.no_probes:
+        # the same B200 schedule on a 24 GiB pool: evictions + restores + a drop
+        other = summary("llama8b_b200", "llama8b_b200: the headline workload on a 24 GiB KV pool (memory pressure: "
+                                        "eviction, checkpoint, restore, layer-wise drop)")
+        if args.h100:
+            h100 = summary("llama8b", "llama8b: reference 8B preset oracle (H100-calibrated schedule), 24 GiB pool")
     tr, K, res, s0, s1 = rp["tr"], rp["K"], rp["res"], rp["s0"], rp["s1"]
     if args.dump and rank == 0:
         shapes = []
@@ -484,9 +494,9 @@ def main():
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": (f"{main_trace}: Llama-3.1-8B shape bf16, 1 B200 per rank, the reference's ConServe "
                                 "co-serving run (bursty online Gamma rate 3/s cv 2, 4096/256, 30 s + 64-request "
-                                "offline backlog with replenish, chunked prefill, 24 GiB KV pool, safepoint every "
-                                "layer)" + (", scheduled with the reference's own fit of the B200-measured latency "
-                                            "grid (profiles/b200_fit.json)" if main_trace.endswith("b200") else ""))
+                                "offline backlog with replenish, chunked prefill, the reference's default 60 GiB KV "
+                                "pool, safepoint every layer), scheduled with the reference's own fit of the "
+                                "B200-measured latency grid (profiles/b200_fit.json)")
                    if main_trace.startswith("llama8b") else
                    (f"{main_trace}: Qwen-2.5-14B shape bf16 (48 layers, 40/8 heads) on ONE B200, bursty online "
                     "2 req/s cv 2 (4096/256, 30 s) + 64-request offline backlog, 40 GiB KV pool, TBT SLO 200 ms, "
@@ -509,7 +519,8 @@ def main():
                         frac_d2h=(host_link["d2h_gbs"] or 0) / link_peak["d2h"],
                         frac_h2d=(host_link["h2d_gbs"] or 0) / link_peak["h2d"]),
         "nonresident_reads": nonres,
-        "h100_schedule": other,
+        "memory_pressure": other,
+        "h100_schedule": h100,
         "roofline": {"kernel": "attn_decode_kernel<128,4> (K1)", "bound": "hbm", "achieved": dec.get("gbs"),
                      "peak": hbm_peak, "unit": "GB/s", "frac": dec.get("frac"),
                      "traffic": traffic.get("K1", {}).get("dram_bytes"),

@@ -84,6 +84,13 @@ def scenario(name: str):
         # the scheduler budgets TBT x (1 - margin) (config.hpp:17-28)
         cfg["slo"]["safety_margin"] = 0.2
         return cfg, None
+    if name == "llama8b_b200_kv60":
+        # the same B200 schedule with the reference's default 60 GiB KV pool
+        # (config.hpp:37): offline requests stay resident (no restores), every
+        # new KV token is still checkpointed
+        cfg, _ = scenario("llama8b_b200")
+        cfg["cluster"]["gpu_kv_capacity"] = 60 << 30
+        return cfg, None
     if name == "qwen14b_b200":
         # BASELINE config 3's model (Qwen-2.5-14B shape: 48 layers, 40/8 heads,
         # 196608 B/token -- the reference presets' own KV unit) on ONE B200,
