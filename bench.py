@@ -442,7 +442,7 @@ def main():
     if args.workload == "llama8b" and not args.no_probes:
         # the same B200 schedule on a 24 GiB pool: evictions + restores + a drop
         other = summary("llama8b_b200", "llama8b_b200: the headline workload on a 24 GiB KV pool (memory pressure: "
-                                        "eviction, checkpoint, restore, layer-wise drop)")
+                                        "eviction, checkpoint and restore)")
         if args.h100:
             h100 = summary("llama8b", "llama8b: reference 8B preset oracle (H100-calibrated schedule), 24 GiB pool")
     tr, K, res, s0, s1 = rp["tr"], rp["K"], rp["res"], rp["s0"], rp["s1"]
