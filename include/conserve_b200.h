@@ -117,6 +117,17 @@ int cs_destroy(cs_engine* e);
  * caller broadcasts the 128 bytes, every rank calls cs_nccl_init. */
 int cs_nccl_unique_id(uint8_t out_id[128]);
 int cs_nccl_init(cs_engine* e, const uint8_t id[128]);
+/* Peer-memory all-reduce instead of NCCL: one kernel per
+ * o_proj / down-proj reads every rank's partial buffer directly over NVLink
+ * (device-side step flags; graph-safe). Each rank exports its exchange
+ * region (cs_tp_exchange_ipc_handle, 64 bytes; the caller all-gathers them)
+ * and attaches all ranks' regions in rank order (cs_tp_attach_ipc). Ranks in
+ * one process (cs_tp_exchange_ptr / cs_tp_attach_peers) may share a device:
+ * same_device != 0 keeps the spinning kernel small (loopback tests). */
+int cs_tp_exchange_ptr(cs_engine* e, void** out);
+int cs_tp_exchange_ipc_handle(cs_engine* e, uint8_t out[64]);
+int cs_tp_attach_peers(cs_engine* e, void* const* peers, int32_t n, int32_t same_device);
+int cs_tp_attach_ipc(cs_engine* e, const uint8_t* handles, int32_t n);
 
 /* ------------------------------------------- KV block pool (C1 + C2 rows) -- */
 /* Mirrors coserve::AllocResult / EvictStats / ResumeCost / TransferJob /

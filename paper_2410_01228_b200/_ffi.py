@@ -115,6 +115,10 @@ EXPORTS = {
     "cs_destroy": ([E], C.c_int),
     "cs_nccl_unique_id": ([P(C.c_uint8)], C.c_int),
     "cs_nccl_init": ([E, P(C.c_uint8)], C.c_int),
+    "cs_tp_exchange_ptr": ([E, P(C.c_void_p)], C.c_int),
+    "cs_tp_exchange_ipc_handle": ([E, P(C.c_uint8)], C.c_int),
+    "cs_tp_attach_peers": ([E, P(C.c_void_p), C.c_int32, C.c_int32], C.c_int),
+    "cs_tp_attach_ipc": ([E, P(C.c_uint8), C.c_int32], C.c_int),
     "cs_kv_register_request": ([E, C.c_int64, C.c_int32], C.c_int),
     "cs_kv_allocate": ([E, C.c_int64, C.c_int64, C.c_int64, P(cs_alloc_result)], C.c_int),
     "cs_kv_commit": ([E, C.c_int64], C.c_int),

@@ -71,6 +71,16 @@ struct AttnParams {
   float scale_log2;             // softmax_scale * log2(e)
 };
 
+// Peer-memory all-reduce arguments (kernels.cu p2p_allreduce): for each of
+// the g ranks, the partial buffer of this step and its exchange-region words.
+struct P2PArgs {
+  const __nv_bfloat16* part[8];
+  uint64_t* flag[8];   // published step of each rank
+  uint64_t* step[8];   // step counter of each rank (only step[rank] is used)
+  int* arrive;         // this rank's block-arrival counter
+  int32_t rank, g;
+};
+
 __host__ __device__ inline uint64_t mix64(uint64_t x) {
   x += 0x9e3779b97f4a7c15ULL;
   x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;

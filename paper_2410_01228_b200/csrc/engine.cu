@@ -56,6 +56,7 @@ void fill_pool(__nv_bfloat16* pool, size_t n, uint64_t seed, cudaStream_t s);
 bool launch_attention(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_dec_grid,
                       int n_pt_grid, cudaStream_t s);
 int prefill_tile_rows();
+void p2p_allreduce(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s);
 }  // namespace csk
 
 namespace {
@@ -302,6 +303,26 @@ struct cs_engine {
   }
   void gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
   void allreduce(__nv_bfloat16* buf, int64_t count);
+  // ---- peer-memory all-reduce: exchange region =
+  // [2 partial buffers of (max_tok*hidden + 64) bf16][flag u64][step u64][arrive i32]
+  uint8_t* xchg = nullptr;
+  size_t xchg_part_elems = 0;
+  bool p2p = false;
+  int p2p_blocks = 0;
+  int part_slot = 0;                   // next partial buffer (same sequence on every rank)
+  std::vector<uint8_t*> peer_xchg;     // exchange region of every rank, rank order
+  std::vector<cudaIpcMemHandle_t> opened;  // (for cs_destroy) handles we opened
+  std::vector<void*> opened_ptrs;
+  __nv_bfloat16* xpart(uint8_t* base, int slot) const {
+    return reinterpret_cast<__nv_bfloat16*>(base) + static_cast<size_t>(slot) * xchg_part_elems;
+  }
+  uint64_t* xflag(uint8_t* base) const {
+    return reinterpret_cast<uint64_t*>(base + 2 * xchg_part_elems * sizeof(__nv_bfloat16));
+  }
+  // destination of a partial-sum GEMM: this rank's next exchange buffer when
+  // the peer path is attached, else the all-reduce buffer itself (NCCL, g=1)
+  __nv_bfloat16* partial_out(__nv_bfloat16* buf) { return p2p ? xpart(xchg, part_slot) : buf; }
+  void reduce_into(__nv_bfloat16* buf, int64_t count);
 };
 
 namespace {
@@ -503,7 +524,29 @@ void cs_engine::gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, in
 
 void cs_engine::allreduce(__nv_bfloat16* buf, int64_t count) {
   if (tp <= 1 || count <= 0) return;
+  if (!comm) throw std::logic_error("tp_size > 1 needs cs_nccl_init or cs_tp_attach_* before a forward");
   CKN(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclBfloat16, ncclSum, comm, s_compute));
+}
+
+// Sums the partial written by the preceding partial_out() GEMM over all ranks
+// into buf (peer path) or reduces buf in place (NCCL).
+void cs_engine::reduce_into(__nv_bfloat16* buf, int64_t count) {
+  if (tp <= 1 || count <= 0) return;
+  if (!p2p) {
+    allreduce(buf, count);
+    return;
+  }
+  csk::P2PArgs a{};
+  for (int r = 0; r < tp; ++r) {
+    a.part[r] = xpart(peer_xchg[static_cast<size_t>(r)], part_slot);
+    a.flag[r] = xflag(peer_xchg[static_cast<size_t>(r)]);
+    a.step[r] = xflag(peer_xchg[static_cast<size_t>(r)]) + 1;
+  }
+  a.arrive = reinterpret_cast<int*>(xflag(xchg) + 2);
+  a.rank = rank;
+  a.g = tp;
+  csk::p2p_allreduce(a, buf, count, p2p_blocks, s_compute);
+  part_slot ^= 1;
 }
 
 // GEMM rows for a layer: all token rows until the host has observed a drop.
@@ -558,19 +601,28 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
     ap.layer = l;
     if (!csk::launch_attention(ap, &kv_map, D, G, graph ? Tg : it.n_dec, it.n_pt, s_compute))
       throw ConfigError("unsupported attention shape");
-    gemm(attn, w.wo[l], tmp, static_cast<int>(M), hidden, hq * D, false);
-    allreduce(tmp, M * hidden);
+    {
+      __nv_bfloat16* part = partial_out(tmp);
+      gemm(attn, w.wo[l], part, static_cast<int>(M), hidden, hq * D, false);
+      if (part != tmp) ++n_launch;
+      reduce_into(tmp, M * hidden);
+    }
     csk::add_rmsnorm(x, tmp, w.mlp_norm[l], xn, hidden, cfg.rms_eps, desc, nullptr, T, s_compute);
     gemm(xn, w.wgu[l], gu, static_cast<int>(M), 2 * ffn, hidden, false);
     csk::silu_mul(gu, act, ffn, desc, T, s_compute);
-    gemm(act, w.wd[l], tmp, static_cast<int>(M), hidden, ffn, false);
-    if (tp > 1) {
-      if (is_sp(l + 1)) {
-        csk::safepoint_vote(tmp + M * hidden, desc, mailbox_dev, s_compute);
-        allreduce(tmp, M * hidden + 8);
-        CK(cudaMemcpyAsync(tail, tmp + M * hidden, 16, cudaMemcpyDeviceToDevice, s_compute));
-      } else {
-        allreduce(tmp, M * hidden);
+    {
+      __nv_bfloat16* part = partial_out(tmp);
+      gemm(act, w.wd[l], part, static_cast<int>(M), hidden, ffn, false);
+      if (tp > 1) {
+        if (part != tmp) ++n_launch;
+        if (is_sp(l + 1)) {
+          // the safepoint vote rides in 8 extra elements of this all-reduce
+          csk::safepoint_vote(part + M * hidden, desc, mailbox_dev, s_compute);
+          reduce_into(tmp, M * hidden + 8);
+          CK(cudaMemcpyAsync(tail, tmp + M * hidden, 16, cudaMemcpyDeviceToDevice, s_compute));
+        } else {
+          reduce_into(tmp, M * hidden);
+        }
       }
     }
     n_launch += (l == 0 ? 1 : 0) + (is_sp(l) ? 1 : 0) + 4 + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
@@ -1052,6 +1104,12 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         CK(cudaMalloc(&e->attn, T * e->hq * e->D * 2));
         CK(cudaMalloc(&e->tmp, (T * H + 64) * 2));
         CK(cudaMemset(e->tmp, 0, (T * H + 64) * 2));
+        if (e->tp > 1) {  // peer all-reduce exchange region (own allocation: IPC-exportable)
+          e->xchg_part_elems = static_cast<size_t>(T * H + 64);
+          const size_t xb = 2 * e->xchg_part_elems * 2 + 64;
+          CK(cudaMalloc(&e->xchg, xb));
+          CK(cudaMemset(e->xchg, 0, xb));
+        }
         CK(cudaMalloc(&e->gu, T * 2 * e->ffn * 2));
         CK(cudaMalloc(&e->act, T * e->ffn * 2));
         CK(cudaMalloc(&e->xl, e->max_ent * H * 2));
@@ -1122,6 +1180,8 @@ int cs_destroy(cs_engine* e) {
       }
       if (e->lt) cublasLtDestroy(e->lt);
       if (e->comm) ncclCommDestroy(e->comm);
+      for (void* p : e->opened_ptrs) cudaIpcCloseMemHandle(p);
+      if (e->xchg) cudaFree(e->xchg);
       cudaFree(e->kv);
       cudaFreeHost(e->host_kv);
       for (auto& r : e->ring) cudaFreeHost(r.host);
@@ -1165,6 +1225,64 @@ int cs_nccl_init(cs_engine* e, const uint8_t id[128]) {
     std::memcpy(&nid, id, 128);
     CK(cudaSetDevice(e->cfg.device));
     CKN(ncclCommInitRank(&e->comm, e->tp, nid, e->rank));
+  });
+}
+
+int cs_tp_exchange_ptr(cs_engine* e, void** out) {
+  return guard([&] {
+    if (!e->xchg) throw std::logic_error("no exchange region: tp_size must be > 1 with a model");
+    *out = e->xchg;
+  });
+}
+
+int cs_tp_exchange_ipc_handle(cs_engine* e, uint8_t out[64]) {
+  return guard([&] {
+    if (!e->xchg) throw std::logic_error("no exchange region: tp_size must be > 1 with a model");
+    cudaIpcMemHandle_t h;
+    static_assert(sizeof(h) == 64, "ipc handle size");
+    CK(cudaIpcGetMemHandle(&h, e->xchg));
+    std::memcpy(out, &h, 64);
+  });
+}
+
+static void attach_common(cs_engine* e, const std::vector<uint8_t*>& peers, bool same_device) {
+  if (static_cast<int>(peers.size()) != e->tp) throw std::invalid_argument("need one exchange region per rank");
+  if (e->tp > 8) throw std::invalid_argument("peer all-reduce supports up to 8 ranks");
+  if (peers[static_cast<size_t>(e->rank)] != e->xchg) throw std::invalid_argument("own exchange region out of place");
+  e->peer_xchg = peers;
+  e->p2p = true;
+  e->part_slot = 0;
+  // same-device (loopback) peers run concurrently with this kernel's
+  // spinning blocks: keep it small so the other rank's kernels get SMs
+  e->p2p_blocks = same_device ? 16 : 2 * e->sms;
+  e->drop_graphs();
+}
+
+int cs_tp_attach_peers(cs_engine* e, void* const* peers, int32_t n, int32_t same_device) {
+  return guard([&] {
+    std::vector<uint8_t*> v;
+    for (int i = 0; i < n; ++i) v.push_back(static_cast<uint8_t*>(peers[i]));
+    attach_common(e, v, same_device != 0);
+  });
+}
+
+int cs_tp_attach_ipc(cs_engine* e, const uint8_t* handles, int32_t n) {
+  return guard([&] {
+    std::vector<uint8_t*> v(static_cast<size_t>(n), nullptr);
+    CK(cudaSetDevice(e->cfg.device));
+    for (int i = 0; i < n; ++i) {
+      if (i == e->rank) {
+        v[static_cast<size_t>(i)] = e->xchg;
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + 64 * i, 64);
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      e->opened_ptrs.push_back(p);
+      v[static_cast<size_t>(i)] = static_cast<uint8_t*>(p);
+    }
+    attach_common(e, v, false);
   });
 }
 

@@ -2,6 +2,7 @@
 // append (K3), the preemption safepoint (K6) and the checkpoint gather /
 // restore scatter over the host link (K4 / K5).
 #include <algorithm>
+#include <cstdio>
 
 #include "common.cuh"
 
@@ -412,6 +413,95 @@ __global__ void fill_pool_kernel(__nv_bfloat16* pool, size_t n, uint64_t seed) {
 }
 void fill_pool(__nv_bfloat16* pool, size_t n, uint64_t seed, cudaStream_t s) {
   fill_pool_kernel<<<2048, 256, 0, s>>>(pool, n, seed);
+}
+
+}  // namespace csk
+
+namespace csk {
+
+// ------------------------------------------ peer-memory all-reduce (C-1) ----
+// KV-head-group sharding: the o_proj / down-proj partial sums
+// of the g ranks are added by one kernel that reads every rank's partial
+// buffer directly (NVLink peer memory across GPUs; the same device in the
+// loopback test) -- no NCCL launch, no staging copy. Ordering is device-side
+// so a captured CUDA graph replays correctly:
+//   * each rank keeps a step counter in its exchange region; every block
+//     reads seq = step + 1;
+//   * block 0 publishes flag[rank] = seq (release, system scope) -- the GEMM
+//     that wrote this rank's partial precedes this kernel on the stream;
+//   * every block waits (acquire, system scope) until all peers' flags reach
+//     seq, sums its chunk of the g partials in fp32 and writes bf16;
+//   * the last block to finish stores step = seq.
+// Partials alternate between two buffers per rank (host-chosen, the same
+// sequence on every rank), so a partial is never overwritten while a peer can
+// still be reading it. A bounded spin (2 s) traps instead of hanging.
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(256) p2p_allreduce_kernel(P2PArgs a, __nv_bfloat16* out, int64_t count) {
+  __shared__ uint64_t s_seq;
+  __shared__ int s_last;
+  if (threadIdx.x == 0) s_seq = *reinterpret_cast<volatile uint64_t*>(a.step[a.rank]) + 1;
+  __syncthreads();
+  const uint64_t seq = s_seq;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(a.flag[a.rank], seq);
+  }
+  if (threadIdx.x < a.g) {
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_sys(a.flag[threadIdx.x]) < seq) {
+      if (globaltimer_ns() - t0 > 2000000000ull) {
+        printf("p2p_allreduce: rank %d timed out waiting for rank %d (seq %llu, its flag %llu, its step %llu)\n",
+               a.rank, threadIdx.x, static_cast<unsigned long long>(seq),
+               static_cast<unsigned long long>(ld_acquire_sys(a.flag[threadIdx.x])),
+               static_cast<unsigned long long>(ld_acquire_sys(a.step[threadIdx.x])));
+        __trap();
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t nv = count / 8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nv;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int p = 0; p < a.g; ++p) {
+      const uint4 v = __ldcv(reinterpret_cast<const uint4*>(a.part[p]) + i);
+      const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(e[j]);
+    }
+    uint4 o;
+    __nv_bfloat16* oe = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) oe[j] = __float2bfloat16(acc[j]);
+    reinterpret_cast<uint4*>(out)[i] = o;
+  }
+  if (blockIdx.x == 0) {  // tail (count % 8)
+    for (int64_t i = nv * 8 + threadIdx.x; i < count; i += blockDim.x) {
+      float acc = 0.f;
+      for (int p = 0; p < a.g; ++p) acc += __bfloat162float(a.part[p][i]);
+      out[i] = __float2bfloat16(acc);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(a.arrive, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    *a.arrive = 0;
+    *reinterpret_cast<volatile uint64_t*>(a.step[a.rank]) = seq;
+  }
+}
+
+void p2p_allreduce(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s) {
+  if (count <= 0) return;
+  p2p_allreduce_kernel<<<blocks, 256, 0, s>>>(a, out, count);
 }
 
 }  // namespace csk

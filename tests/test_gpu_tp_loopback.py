@@ -1,0 +1,147 @@
+"""KV-head-group sharding end to end on ONE device (loopback): two rank
+engines (tp_size=2) share GPU 0 and exchange their o_proj / down-proj
+partial sums through the peer-memory all-reduce kernel (cs_tp_attach_peers,
+the same kernel that reads NVLink peer memory across GPUs). Checks:
+
+* both ranks produce identical logits (they fold the partials in the same
+  order), within bf16 tolerance of the unsharded engine and the fp32 oracle,
+  for prefill, mixed and decode-only (CUDA-graph) iterations;
+* safepoint agreement: a flag raised on rank 0 ONLY rides the
+  all-reduce as a vote, and both ranks drop the offline entries at the same
+  layer -- no rank runs a collective the other skipped."""
+import ctypes as C
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import paper_2410_01228_b200 as cs
+from oracle import numeric as N
+
+pytestmark = pytest.mark.gpu
+
+# Both ranks live in ONE process here, so any host call that synchronises the
+# device (e.g. a lazily loaded kernel module on a rank's first GEMM) would
+# wait on the other rank's spinning all-reduce: each case runs in a child
+# process with eager module loading. (Real ranks are separate processes on
+# separate GPUs, where this cannot happen.)
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _in_child(case):
+    root = os.path.dirname(_HERE)
+    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER",
+               PYTHONPATH=os.pathsep.join([root, os.environ.get("PYTHONPATH", "")]))
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), case], env=env, capture_output=True, text=True,
+                       timeout=300, cwd=os.path.dirname(_HERE))
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
+
+
+SHAPE = dict(num_layers=4, hidden=256, n_heads=8, n_kv_heads=4, head_dim=64, ffn=512, vocab=512,
+             max_batched_tokens=1024, gpu_kv_capacity=4096 * 16 * 2 * 4 * 64 * 2 * 4, safepoint_interval_layers=1)
+
+
+def _engines(instrumented=0):
+    full = cs.Engine(cs.model_config("tiny", instrumented=instrumented, **SHAPE))
+    ranks = [cs.Engine(cs.model_config("tiny", instrumented=instrumented, tp_size=2, tp_rank=r, **SHAPE))
+             for r in range(2)]
+    ptrs = []
+    for e in ranks:
+        p = C.c_void_p()
+        cs.engine._check(cs.lib().cs_tp_exchange_ptr(e._h, C.byref(p)))
+        ptrs.append(p.value)
+    arr = (C.c_void_p * 2)(*ptrs)
+    for e in ranks:
+        cs.engine._check(cs.lib().cs_tp_attach_peers(e._h, arr, 2, 1))
+    return full, ranks
+
+
+def _all(engs, fn):
+    return [fn(e) for e in engs]
+
+
+def _step(engs, plan, allocs, epoch, signal_rank=None):
+    for e in engs:
+        for be, n in zip(plan, allocs):
+            assert e.allocate(be.request_id, n).ok
+    for e in engs:
+        e.forward_launch(plan, epoch)
+    if signal_rank is not None:
+        engs[signal_rank].preempt_signal(epoch)
+    return [e.iter_wait(want_logits=True) for e in engs]
+
+
+def test_two_ranks_on_one_device_match_unsharded():
+    _in_child("match")
+
+
+def test_flag_on_one_rank_drops_both_at_the_same_layer():
+    _in_child("flag")
+
+
+def case_match():
+    full, ranks = _engines()
+    engs = [full] + ranks
+    orc = N.Oracle(N.ModelShape.from_cfg(full.cfg))
+    try:
+        for e in engs:
+            for r in range(4):
+                e.register_request(r, r == 0)
+        known = {0: 0, 1: 0, 2: 0, 3: 0}
+        prompts = {0: 40, 1: 75, 2: 130, 3: 33}
+        for it in range(6):
+            plan, allocs = [], []
+            for r in range(4):
+                c = known[r]
+                if c < prompts[r]:
+                    plan.append(cs.BatchEntry(r, prompts[r] - c, c, cs.CS_PREFILL, r == 0))
+                    allocs.append(prompts[r] - c + 1)
+                else:
+                    plan.append(cs.BatchEntry(r, 1, c, cs.CS_DECODE, r == 0))
+                    allocs.append(1)
+            outs = _step(engs, plan, allocs, 100 + it)
+            ref = orc.forward([N.Entry(b.request_id, b.compute_tokens, b.context_tokens, b.kind, b.online) for b in plan])
+            (_, lf), (_, l0), (_, l1) = outs
+            assert np.array_equal(l0, l1)                  # ranks agree exactly
+            assert float(np.max(np.abs(l0 - lf))) <= 2e-2  # sharded vs unsharded (bf16 partial sums)
+            assert float(np.max(np.abs(l0 - ref))) <= 2e-2
+            for e in engs:
+                for b in plan:
+                    e.commit_allocations(b.request_id)
+            for b, n in zip(plan, allocs):
+                known[b.request_id] += n
+    finally:
+        for e in engs:
+            e.close()
+
+
+def case_flag():
+    full, ranks = _engines(instrumented=1)
+    full.close()
+    try:
+        for e in ranks:
+            e.register_request(0, True)
+            e.register_request(1, False)
+        plan = [cs.BatchEntry(0, 30, 0, cs.CS_PREFILL, True), cs.BatchEntry(1, 900, 0, cs.CS_PREFILL, False)]
+        (i0, _), (i1, _) = _step(ranks, plan, [31, 900], 7, signal_rank=0)
+        assert i0.preempted_at_layer == i1.preempted_at_layer
+        if i0.preempted_at_layer is not None:
+            assert i0.n_outputs == i1.n_outputs == 1
+        for e in ranks:
+            e.commit_allocations(0)
+            if i0.preempted_at_layer is not None:
+                e.rollback_allocations(1)
+            else:
+                e.commit_allocations(1)
+            e.audit()
+    finally:
+        for e in ranks:
+            e.close()
+
+
+if __name__ == "__main__":
+    sys.path.insert(0, os.path.dirname(_HERE))
+    {"match": case_match, "flag": case_flag}[sys.argv[1]]()
+    print("ok")
