@@ -360,6 +360,9 @@ def main():
     ap.add_argument("--no-probes", action="store_true")
     ap.add_argument("--dump", default=None, help="write per-iteration device times + plan shapes (.npz)")
     ap.add_argument("--h100", action="store_true", help="also replay the H100-calibrated (reference preset) schedule")
+    ap.add_argument("--tp", action="store_true",
+                    help="N>1: shard ONE model over the N GPUs by KV-head groups (peer-memory all-reduce over "
+                         "IPC-mapped exchange regions) instead of N replicas")
     ap.add_argument("--workload", default="llama8b", choices=["llama8b", "qwen14b", "llama70b"],
                     help="llama8b: BASELINE config 2 (default, the headline); llama70b: config 4's model and "
                          "online spike on ONE B200 (tests/golden/llama70b_b200)")
@@ -392,11 +395,21 @@ def main():
         tr = R.load(os.path.join(g, "calls.jsonl.gz"), os.path.join(g, "requests.jsonl.gz"))
         K = args.steps if args.steps > 0 else tr.n_iter - W
         K = min(K, tr.n_iter - W)
-        # replicas: every rank replays the whole trace on its own GPU (weak scaling)
+        # replicas: every rank replays the whole trace on its own GPU (weak
+        # scaling); --tp: every rank replays it on its KV-head shard (one model)
         preset = "llama70b" if name.startswith("llama70b") else "qwen14b" if name.startswith("qwen14b") else "llama8b"
-        cfg = R.engine_config_for(tr, preset, device=local, max_entries=256)
+        shard = dict(tp_size=world, tp_rank=rank) if (args.tp and world > 1) else {}
+        cfg = R.engine_config_for(tr, preset, device=local, max_entries=256, **shard)
         t_setup = time.time()
         eng = cs.Engine(cfg)
+        if shard:
+            import ctypes as C
+            h = (C.c_uint8 * 64)()
+            cs.engine._check(cs.lib().cs_tp_exchange_ipc_handle(eng._h, h))
+            handles = [None] * world
+            dist.all_gather_object(handles, bytes(h))
+            allh = (C.c_uint8 * (64 * world)).from_buffer_copy(b"".join(handles))
+            cs.engine._check(cs.lib().cs_tp_attach_ipc(eng._h, allh, world))
         setup_s = time.time() - t_setup
         R.run(eng, tr, 0, W)
         s0 = eng.stats()
@@ -431,7 +444,8 @@ def main():
     def summary(name, what):
         o = replay(name)
         so, s1o = o["s0"], o["s1"]
-        return {"workload": what, "value": world * o["off"] / o["gpu_s"], "e2e": world * o["off"] / o["wall_s"],
+        reps = 1 if args.tp else world
+        return {"workload": what, "value": reps * o["off"] / o["gpu_s"], "e2e": reps * o["off"] / o["wall_s"],
                 "online_p99_tpot_ms": percentile(o["tpot"], 0.99), "online_p99_tbt_ms": percentile(o["tbt"], 0.99),
                 "offline_tokens": o["off"], "steps": int(o["res"].iterations),
                 "d2h_bytes": s1o.moved_d2h_bytes - so.moved_d2h_bytes,
@@ -458,8 +472,9 @@ def main():
     off, on, tpot, tbt = rp["off"], rp["on"], rp["tpot"], rp["tbt"]
     gpu_s, wall_s, clocks, setup_s = rp["gpu_s"], rp["wall_s"], rp["clocks"], rp["setup_s"]
     n = world
-    value = n * off / gpu_s
-    e2e = n * off / wall_s
+    replicas = 1 if args.tp else n  # sharded: one model over all GPUs
+    value = replicas * off / gpu_s
+    e2e = replicas * off / wall_s
     d2h_b = s1.moved_d2h_bytes - s0.moved_d2h_bytes
     d2h_ms = s1.moved_d2h_ms - s0.moved_d2h_ms
     h2d_b = s1.moved_h2d_bytes - s0.moved_h2d_bytes
@@ -490,7 +505,8 @@ def main():
     drops = [(int(l), float(u)) for l, u in zip(res.dropped_layer, res.drop_latency_us) if l >= 0]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": int(res.iterations), "warmup": W,
-        "ms_per_step": 1e3 * gpu_s / max(res.iterations, 1), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * gpu_s / max(res.iterations, 1), "higher_is_better": True,
+        "scaling": "strong" if (args.tp and n > 1) else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": (f"{main_trace}: Llama-3.1-8B shape bf16, 1 B200 per rank, the reference's ConServe "
                                 "co-serving run (bursty online Gamma rate 3/s cv 2, 4096/256, 30 s + 64-request "
@@ -506,7 +522,7 @@ def main():
                     "spike 0.5 -> 2 req/s at 20 s (2048/128) against a 48-request offline backlog, 20 GiB KV pool, "
                     "safepoint every layer, scheduled with the reference's fit of the B200 70B profile "
                     "(profiles/b200_fit_70b.json)"),
-                   "iterations": f"[{W}, {W + K}) of {tr.n_iter}", "parallelism": "replica" if n > 1 else "single",
+                   "iterations": f"[{W}, {W + K}) of {tr.n_iter}", "parallelism": (f"tp{n} (KV-head groups)" if args.tp else "replica") if n > 1 else "single",
                    "l2": "inputs larger than L2 (16 GB of weights + KV per step)"},
         "e2e": {"value": e2e, "unit": UNIT,
                 "h2d_bytes_per_step": float(res.h2d_bytes.mean()) if res.iterations else 0,
