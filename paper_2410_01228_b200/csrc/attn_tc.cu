@@ -66,6 +66,10 @@ constexpr int kKeys = 128;   // keys per tile (UMMA N of S, K of PV)
 constexpr int kStages = 2;   // K/V ring depth
 constexpr int kPage = 16;
 constexpr int kThreads = 320;
+#ifndef CS_K2_POLY
+#define CS_K2_POLY 2  // tools/k2_sweep.py: 2 of 8 beats 0, 3 and 4 (profiles/r1/k2_poly_sweep.md)
+#endif
+constexpr int kPoly8 = CS_K2_POLY;  // score pairs (of every 8) exponentiated by ex2_poly2
 constexpr int kChunkBytes = 128 * 128;        // [128 rows][64 bf16] SWIZZLE_128B chunk (Q) = 16 KB
 constexpr int kKvChunkBytes = kKeys * 128;    // [128 keys][64 bf16] chunk (K, V) = 16 KB
 
@@ -99,10 +103,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int CH = Lay::kChunks;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // blockIdx.x = (rank of the tile in the heaviest-first order) x hkv + KV
+  // head: the block scheduler hands out the longest tiles first
   const int n_pt = p.desc->n_pt_cur;
-  if (static_cast<int>(blockIdx.x) >= n_pt) return;
-  const int tile_idx = n_pt - 1 - static_cast<int>(blockIdx.x);  // latest (heaviest) tiles first
-  const int kvh = blockIdx.y;
+  const int tile_idx = p.tile_order[blockIdx.x / p.hkv];
+  const int kvh = blockIdx.x % p.hkv;
+  if (tile_idx >= n_pt) return;  // an offline tile dropped at a safepoint
   const PrefillTile t = p.tiles[tile_idx];
   const int ent = t.entry;
   const int q0 = p.ent_q0[ent];
@@ -294,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
 #ifdef CS_K2_TIMERS
-      if (lane == 0 && blockIdx.y == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && blockIdx.z == 0)
+      if (lane == 0 && kvh == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - p.hkv) && blockIdx.z == 0)
         printf("K2T mma  cta=%d n_kt=%d total=%lld wait_k=%lld wait_v=%lld wait_p=%lld\n", blockIdx.x, n_kt,
                clock64() - t_begin, t_wk, t_wv, t_wp);
 #endif
@@ -346,15 +352,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         // a split's rows may see no valid key yet (m_used = -inf): p = 0
         const float msub = m_used == -INFINITY ? 0.f : m_used;
         uint32_t pk[kKeys / 2];
-        float rsa[4] = {0.f, 0.f, 0.f, 0.f};
+        // packed fp32x2 FMA / add (FFMA2, FADD2): half the ALU issue slots
+        const float2 sc2 = make_float2(scale, scale), ms2 = make_float2(-msub, -msub);
+        float2 rsa[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int i = 0; i < kKeys; i += 2) {
-          const float p0 = tc::ex2_approx(fmaf(s[i], scale, -msub));
-          const float p1 = tc::ex2_approx(fmaf(s[i + 1], scale, -msub));
-          rsa[(i >> 1) & 3] += p0 + p1;
-          pk[i / 2] = pack_bf16(p0, p1);
+          const float2 x = __ffma2_rn(make_float2(s[i], s[i + 1]), sc2, ms2);
+          // kPoly8 of every 8 pairs on the FMA pipe: the MUFU (16 ex2/clk/SM)
+          // is otherwise as busy as the tensor core
+          const float2 pp = ((i >> 1) & 7) < kPoly8 ? tc::ex2_poly2(x)
+                                                    : make_float2(tc::ex2_approx(x.x), tc::ex2_approx(x.y));
+          rsa[(i >> 1) & 1] = __fadd2_rn(rsa[(i >> 1) & 1], pp);
+          pk[i / 2] = pack_bf16(pp.x, pp.y);
         }
-        const float rs = (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
+        const float rs = (rsa[0].x + rsa[1].x) + (rsa[0].y + rsa[1].y);
         l = l * alpha + rs;
         // tcgen05.ld/st are warp-collective (.sync.aligned): the correction
         // runs for the whole warp if any of its rows needs it (alpha = 1 for
@@ -384,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_arrive(&p_full[qi]);
       }
 #ifdef CS_K2_TIMERS
-      if (r == 0 && blockIdx.y == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && blockIdx.z == 0)
+      if (r == 0 && kvh == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - p.hkv) && blockIdx.z == 0)
         printf("K2T smax cta=%d qi=%d loop=%lld wait_s=%lld wait_o=%lld\n", blockIdx.x, qi, clock64() - t_sbegin,
                t_ws, t_wo);
 #endif
@@ -479,13 +490,15 @@ void launch_prefill_tc_t(const AttnParams& p, const CUtensorMap* kv_map, int n_p
                          TcLayout<D>::launch_bytes);
     attr = true;
   }
-  attn_prefill_tc_kernel<D, G><<<dim3(n_pt_grid, p.hkv, p.k2_splits), kThreads, TcLayout<D>::launch_bytes, s>>>(
+  attn_prefill_tc_kernel<D, G><<<dim3(n_pt_grid * p.hkv, 1, p.k2_splits), kThreads, TcLayout<D>::launch_bytes, s>>>(
       p, *kv_map);
   if (p.k2_splits > 1) attn_prefill_combine_kernel<D, G><<<dim3(n_pt_grid, p.hkv), 256, 0, s>>>(p);
 }
 
 // Rows per K2 work tile (engine.cu builds the tile list with this step).
 int prefill_tile_rows() { return kQT * kRows; }
+// Keys per K2 key tile (the unit of its split-K).
+int prefill_tile_keys() { return kKeys; }
 
 bool launch_prefill_tc(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_pt_grid,
                        cudaStream_t s) {

@@ -62,12 +62,13 @@ struct AttnParams {
   const int32_t* block_table;   // flat
   const int32_t* dec_ent;       // [n_dec] entry index of single-query entries
   const PrefillTile* tiles;     // [n_pt]
+  const int32_t* tile_order;    // [n_pt] K2 launch order: tile indices, most keys first
   float* ws;                    // K1 split-K partials
   int32_t* dec_cnt;             // K1 split-K arrival counters [entry][kv head], self-resetting
   float* ws2;                   // K2 split-K partials [tile][kvh][split] x {O [D][256], m [256], l [256]}
   int32_t layer, num_layers, hq, hkv, qkv_stride;
   int32_t n_splits, pages_per_split;   // K1: splits over pages
-  int32_t k2_splits, k2_tiles_per_split;  // K2: splits over 64-key tiles
+  int32_t k2_splits, k2_tiles_per_split;  // K2: splits over 128-key tiles
   float scale_log2;             // softmax_scale * log2(e)
 };
 

@@ -56,6 +56,7 @@ void fill_pool(__nv_bfloat16* pool, size_t n, uint64_t seed, cudaStream_t s);
 bool launch_attention(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_dec_grid,
                       int n_pt_grid, cudaStream_t s);
 int prefill_tile_rows();
+int prefill_tile_keys();
 void p2p_allreduce(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s);
 }  // namespace csk
 
@@ -703,6 +704,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     std::vector<int32_t> tok_ids, tok_pos, tok_slot, ent_q0(n), ent_qlen(n), ent_kvlen(n), ent_bt(n), ent_last(n);
     std::vector<int32_t> dec_ent, bt;
     std::vector<csk::PrefillTile> tiles;
+    std::vector<int32_t> tile_keys;  // keys a tile's rows attend to (K2 work per KV head)
     bool seen_offline = false;
     int n_tok_on = 0, n_ent_on = 0, n_dec_on = 0, n_pt_on = 0, max_dec_pages = 0, max_pre_kv = 0;
     for (int i = 0; i < n; ++i) {
@@ -756,7 +758,11 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
         const int rows = static_cast<int>(pos.size()) * e->G;
         max_pre_kv = std::max(max_pre_kv, kv_len);
         const int step = csk::prefill_tile_rows();
-        for (int r0 = 0; r0 < rows; r0 += step) tiles.push_back({i, r0});
+        for (int r0 = 0; r0 < rows; r0 += step) {
+          tiles.push_back({i, r0});
+          const int last = std::min(r0 + step, rows) - 1;
+          tile_keys.push_back(std::min(kv_len, pos[static_cast<size_t>(last / e->G)] + 1));
+        }
       }
       if (be.online) {
         n_tok_on = static_cast<int>(tok_pos.size());
@@ -838,7 +844,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     const size_t o_tok = region(sizeof(int32_t) * 3 * static_cast<size_t>(Tcap));
     const size_t o_ent = region(sizeof(int32_t) * 5 * E);
     const size_t o_dec = region(sizeof(int32_t) * static_cast<size_t>(Dcap) + 4);
-    const size_t o_tiles = region(sizeof(csk::PrefillTile) * tiles.size() + 8);
+    const size_t o_tiles = region((sizeof(csk::PrefillTile) + 4) * tiles.size() + 8);
     const size_t o_bt = region(sizeof(int32_t) * bt.size() + 4);
     const size_t total = off;
     if (total > e->meta_cap) {
@@ -875,19 +881,28 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     std::memcpy(he + 3 * E, ent_bt.data(), 4 * n);
     std::memcpy(he + 4 * E, ent_last.data(), 4 * n);
     if (!dec_ent.empty()) std::memcpy(h + o_dec, dec_ent.data(), 4 * dec_ent.size());
-    if (!tiles.empty()) std::memcpy(h + o_tiles, tiles.data(), sizeof(csk::PrefillTile) * tiles.size());
+    if (!tiles.empty()) {
+      // K2 launch order: heaviest tiles first (the block scheduler then runs a
+      // longest-first list schedule over the SMs); ties keep plan order
+      std::vector<int32_t> order(tiles.size());
+      for (size_t k = 0; k < order.size(); ++k) order[k] = static_cast<int32_t>(k);
+      std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return tile_keys[a] > tile_keys[b]; });
+      std::memcpy(h + o_tiles, tiles.data(), sizeof(csk::PrefillTile) * tiles.size());
+      std::memcpy(h + o_tiles + sizeof(csk::PrefillTile) * tiles.size(), order.data(), 4 * order.size());
+    }
     std::memcpy(h + o_bt, bt.data(), 4 * bt.size());
 
     // split-K for K2 when the tile grid cannot fill the SMs (few prefill rows
-    // over a long context): splits of >= 8 key tiles (512 keys), <= 64
+    // over a long context): ctas x splits <= SMs (one wave), splits of >= 4
+    // key tiles (512 keys), <= 64
     it.k2_splits = 1;
     it.k2_tps = 1 << 30;
     if (it.n_pt > 0) {
       const int ctas = it.n_pt * e->hkv;
-      const int max_kt = (max_pre_kv + 63) / 64;
-      if (ctas < e->sms && max_kt >= 16) {
-        int S2 = (e->sms + ctas - 1) / ctas;
-        S2 = std::min({S2, max_kt / 8, 64});
+      const int kt = csk::prefill_tile_keys();
+      const int max_kt = (max_pre_kv + kt - 1) / kt;
+      if (ctas < e->sms && max_kt >= 8) {
+        const int S2 = std::min({e->sms / ctas, max_kt / 4, 64});
         if (S2 > 1) {
           it.k2_tps = (max_kt + S2 - 1) / S2;
           it.k2_splits = (max_kt + it.k2_tps - 1) / it.k2_tps;
@@ -918,6 +933,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     ap.block_table = reinterpret_cast<const int32_t*>(d + o_bt);
     ap.dec_ent = reinterpret_cast<const int32_t*>(d + o_dec);
     ap.tiles = reinterpret_cast<const csk::PrefillTile*>(d + o_tiles);
+    ap.tile_order = reinterpret_cast<const int32_t*>(d + o_tiles + sizeof(csk::PrefillTile) * tiles.size());
     ap.ws = e->ws;
     ap.dec_cnt = e->dec_cnt;
     ap.num_layers = e->L;
@@ -1123,6 +1139,30 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         CK(cudaMalloc(&e->blas_ws, 64u << 20));
         CKB(cublasSetWorkspace(e->blas, e->blas_ws, 64u << 20));
         CKB(cublasSetMathMode(e->blas, CUBLAS_DEFAULT_MATH));
+        CKB(cublasLtCreate(&e->lt));
+        // Workspaces and the metadata buffer at their upper bounds, so no
+        // iteration frees device memory (cudaFree synchronises the device:
+        // it would stall the copy streams, and deadlock TP ranks that share
+        // a device while a peer spins in the all-reduce).
+        //   K1 splits: rows*hkv*splits < 2 * (4 * sms) whenever splits > 1
+        //   K2 splits: tiles*hkv*splits < 2 * sms whenever splits > 1
+        e->ws_floats = static_cast<size_t>(2 * 4 * e->sms) * e->G * (2 + e->D);
+        CK(cudaMalloc(&e->ws, e->ws_floats * 4));
+        e->ws2_floats = static_cast<size_t>(2 * e->sms) * (e->D + 2) * 256;
+        CK(cudaMalloc(&e->ws2, e->ws2_floats * 4));
+        const size_t E = static_cast<size_t>(e->max_ent);
+        const size_t tiles_max = static_cast<size_t>(T) * e->G / 256 + E + 1;
+        e->meta_cap = align_up(sizeof(csk::IterDesc) + 12 * static_cast<size_t>(T) + 24 * E + 4 +
+                                   (sizeof(csk::PrefillTile) + 4) * (tiles_max + 1) +
+                                   4 * (static_cast<size_t>(pc.n_blocks) + E + 1) + 8 * 16,
+                               1 << 20);
+        CK(cudaMalloc(&e->d_meta, e->meta_cap));
+        CK(cudaMallocHost(&e->h_meta, e->meta_cap));
+        // cuBLASLt algorithm choice for every decode-graph bucket now, at
+        // start-up, instead of inside the first iteration of each bucket
+        const char* nt = std::getenv("CS_NO_GEMM_TUNE");
+        if (e->graphs_enabled && !(nt && nt[0] == '1'))
+          for (int b = 8; b <= 256 && b <= e->max_ent && b <= e->max_tok; b *= 2) e->tune_gemms(b);
       }
       CK(cudaStreamSynchronize(e->s_compute));
       // globaltimer <-> CLOCK_MONOTONIC offset (preemption latency probe)

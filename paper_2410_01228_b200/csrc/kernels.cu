@@ -173,8 +173,8 @@ void silu_mul(const __nv_bfloat16* gu, __nv_bfloat16* act, int ffn, const IterDe
 // scatters k, v into the token's (block, slot) of this layer of the pool.
 // One CTA per token: the D/2 (cos, sin) pairs of the token's position are
 // computed once (accurate sincosf: positions reach 64K) and shared by all
-// Hq + Hkv heads; rotations move bf16x2 pairs, v moves 16-B vectors.
-__global__ void __launch_bounds__(256) rope_append_kernel(__nv_bfloat16* qkv, const int32_t* tok_pos,
+// Hq + Hkv heads; rotations and the v copy move 16-B vectors (D % 16 == 0).
+__global__ void __launch_bounds__(128) rope_append_kernel(__nv_bfloat16* qkv, const int32_t* tok_pos,
                                                           const int32_t* tok_slot, __nv_bfloat16* pool, int hq,
                                                           int hkv, int D, int num_layers, int layer, float theta,
                                                           const IterDesc* desc) {
@@ -196,18 +196,29 @@ __global__ void __launch_bounds__(256) rope_append_kernel(__nv_bfloat16* qkv, co
   const int blk = slot >> 4, off = slot & 15;
   const size_t layer_elems = static_cast<size_t>(2) * hkv * 16 * D;
   __nv_bfloat16* kv_base = pool + (static_cast<size_t>(blk) * num_layers + layer) * layer_elems;
-  const int pairs = half / 2;  // bf16x2 pairs per half-row
-  for (int i = threadIdx.x; i < (hq + hkv) * pairs; i += blockDim.x) {
-    const int h = i / pairs, j = (i % pairs) * 2;
+  // 8 consecutive (j .. j+7) rotation pairs per thread: 16-B loads of both halves
+  const int chunks = half / 8;
+  for (int i = threadIdx.x; i < (hq + hkv) * chunks; i += blockDim.x) {
+    const int h = i / chunks, j = (i % chunks) * 8;
     __nv_bfloat16* hp = row + h * D;
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(hp + j));
-    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(hp + j + half));
-    const float2 r0 = rot[j], r1 = rot[j + 1];
-    const __nv_bfloat162 y1 = __floats2bfloat162_rn(a.x * r0.x - b.x * r0.y, a.y * r1.x - b.y * r1.y);
-    const __nv_bfloat162 y2 = __floats2bfloat162_rn(b.x * r0.x + a.x * r0.y, b.y * r1.x + a.y * r1.y);
+    const uint4 ua = *reinterpret_cast<const uint4*>(hp + j);
+    const uint4 ub = *reinterpret_cast<const uint4*>(hp + j + half);
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&ua);
+    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&ub);
+    uint4 uy1, uy2;
+    __nv_bfloat162* y1 = reinterpret_cast<__nv_bfloat162*>(&uy1);
+    __nv_bfloat162* y2 = reinterpret_cast<__nv_bfloat162*>(&uy2);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 a = __bfloat1622float2(a2[k]);
+      const float2 b = __bfloat1622float2(b2[k]);
+      const float2 r0 = rot[j + 2 * k], r1 = rot[j + 2 * k + 1];
+      y1[k] = __floats2bfloat162_rn(a.x * r0.x - b.x * r0.y, a.y * r1.x - b.y * r1.y);
+      y2[k] = __floats2bfloat162_rn(b.x * r0.x + a.x * r0.y, b.y * r1.x + a.y * r1.y);
+    }
     __nv_bfloat16* dst = h < hq ? hp : kv_base + (static_cast<size_t>(h - hq) * 16 + off) * D;
-    *reinterpret_cast<__nv_bfloat162*>(dst + j) = y1;
-    *reinterpret_cast<__nv_bfloat162*>(dst + j + half) = y2;
+    *reinterpret_cast<uint4*>(dst + j) = uy1;
+    *reinterpret_cast<uint4*>(dst + j + half) = uy2;
   }
   // v rows: straight copy, 16 bytes per thread
   const __nv_bfloat16* v = row + (hq + hkv) * D;
@@ -222,7 +233,7 @@ void rope_append(__nv_bfloat16* qkv, const int32_t* tok_pos, const int32_t* tok_
                  int hkv, int D, int num_layers, int layer, float theta, const IterDesc* desc, int grid,
                  cudaStream_t s) {
   if (grid > 0)
-    rope_append_kernel<<<grid, 256, 0, s>>>(qkv, tok_pos, tok_slot, pool, hq, hkv, D, num_layers, layer, theta, desc);
+    rope_append_kernel<<<grid, 128, 0, s>>>(qkv, tok_pos, tok_slot, pool, hq, hkv, D, num_layers, layer, theta, desc);
 }
 
 // ---------------------------------------------------------------- argmax ----

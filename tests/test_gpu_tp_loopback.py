@@ -34,9 +34,15 @@ def _in_child(case):
     root = os.path.dirname(_HERE)
     env = dict(os.environ, CUDA_MODULE_LOADING="EAGER",
                PYTHONPATH=os.pathsep.join([root, os.environ.get("PYTHONPATH", "")]))
-    r = subprocess.run([sys.executable, os.path.abspath(__file__), case], env=env, capture_output=True, text=True,
-                       timeout=300, cwd=os.path.dirname(_HERE))
-    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
+    p = subprocess.Popen([sys.executable, os.path.abspath(__file__), case], env=env, stdout=subprocess.PIPE,
+                         stderr=subprocess.STDOUT, text=True, cwd=os.path.dirname(_HERE))
+    try:
+        out = p.communicate(timeout=420)[0]
+    except subprocess.TimeoutExpired:
+        p.kill()
+        out = p.communicate()[0]
+        raise AssertionError("child timed out:\n" + out[-6000:])
+    assert p.returncode == 0, out[-6000:]
 
 
 SHAPE = dict(num_layers=4, hidden=256, n_heads=8, n_kv_heads=4, head_dim=64, ffn=512, vocab=512,
@@ -102,6 +108,7 @@ def case_match():
                     plan.append(cs.BatchEntry(r, 1, c, cs.CS_DECODE, r == 0))
                     allocs.append(1)
             outs = _step(engs, plan, allocs, 100 + it)
+            print(f"iteration {it} done", flush=True)
             ref = orc.forward([N.Entry(b.request_id, b.compute_tokens, b.context_tokens, b.kind, b.online) for b in plan])
             (_, lf), (_, l0), (_, l1) = outs
             assert np.array_equal(l0, l1)                  # ranks agree exactly
@@ -142,6 +149,8 @@ def case_flag():
 
 
 if __name__ == "__main__":
+    import faulthandler
+    faulthandler.dump_traceback_later(360, exit=True)  # a hang prints every thread's stack
     sys.path.insert(0, os.path.dirname(_HERE))
     {"match": case_match, "flag": case_flag}[sys.argv[1]]()
     print("ok")
