@@ -446,11 +446,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
-// Split-K merge for K2: one CTA per (tile, KV head), one thread per packed
-// row; partials are [d][row] so every load is coalesced across the rows.
+// Split-K merge for K2: one CTA per (tile, KV head, 32 head dims), one thread
+// per packed row; partials are [d][row] so every load is coalesced across the
+// rows, and the split weights are recomputed per split (no local arrays).
 template <int D, int G>
 __global__ void __launch_bounds__(256) attn_prefill_combine_kernel(AttnParams p) {
-  const int tile = blockIdx.x, kvh = blockIdx.y;
+  const int tile = blockIdx.x, kvh = blockIdx.y, d0 = blockIdx.z * 32;
   if (tile >= p.desc->n_pt_cur) return;
   const PrefillTile t = p.tiles[tile];
   const int ent = t.entry;
@@ -461,25 +462,27 @@ __global__ void __launch_bounds__(256) attn_prefill_combine_kernel(AttnParams p)
   const int r = threadIdx.x;
   float M = -INFINITY;
   for (int sp = 0; sp < S; ++sp) M = fmaxf(M, ws[(sp * (D + 2) + D) * 256 + r]);
-  float w[64];  // S <= 64
+  float o[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) o[i] = 0.f;
   float L = 0.f;
   for (int sp = 0; sp < S; ++sp) {
-    const float m = ws[(sp * (D + 2) + D) * 256 + r];
-    w[sp] = m == -INFINITY ? 0.f : exp2f(m - M);
-    L += w[sp] == 0.f ? 0.f : w[sp] * ws[(sp * (D + 2) + D + 1) * 256 + r];
+    const float* w_sp = ws + sp * (D + 2) * 256;
+    const float m = w_sp[D * 256 + r];
+    if (m == -INFINITY) continue;  // skipped splits may hold stale partials
+    const float w = exp2f(m - M);
+    L += w * w_sp[(D + 1) * 256 + r];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] = fmaf(w, w_sp[(d0 + i) * 256 + r], o[i]);
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;
   __nv_bfloat16* dst = p.out + static_cast<size_t>(p.ent_q0[ent] + gr / G) * p.hq * D +
-                       static_cast<size_t>(kvh * G + gr % G) * D;
-  for (int d = 0; d < D; d += 2) {
-    float o0 = 0.f, o1 = 0.f;
-    for (int sp = 0; sp < S; ++sp) {
-      if (w[sp] == 0.f) continue;  // skipped splits may hold stale partials
-      o0 += w[sp] * ws[(sp * (D + 2) + d) * 256 + r];
-      o1 += w[sp] * ws[(sp * (D + 2) + d + 1) * 256 + r];
-    }
-    *reinterpret_cast<uint32_t*>(dst + d) = pack_bf16(o0 * inv, o1 * inv);
-  }
+                       static_cast<size_t>(kvh * G + gr % G) * D + d0;
+#pragma unroll
+  for (int i = 0; i < 32; i += 8)
+    *reinterpret_cast<uint4*>(dst + i) =
+        make_uint4(pack_bf16(o[i] * inv, o[i + 1] * inv), pack_bf16(o[i + 2] * inv, o[i + 3] * inv),
+                   pack_bf16(o[i + 4] * inv, o[i + 5] * inv), pack_bf16(o[i + 6] * inv, o[i + 7] * inv));
 }
 
 template <int D, int G>
@@ -492,7 +495,7 @@ void launch_prefill_tc_t(const AttnParams& p, const CUtensorMap* kv_map, int n_p
   }
   attn_prefill_tc_kernel<D, G><<<dim3(n_pt_grid * p.hkv, 1, p.k2_splits), kThreads, TcLayout<D>::launch_bytes, s>>>(
       p, *kv_map);
-  if (p.k2_splits > 1) attn_prefill_combine_kernel<D, G><<<dim3(n_pt_grid, p.hkv), 256, 0, s>>>(p);
+  if (p.k2_splits > 1) attn_prefill_combine_kernel<D, G><<<dim3(n_pt_grid, p.hkv, D / 32), 256, 0, s>>>(p);
 }
 
 // Rows per K2 work tile (engine.cu builds the tile list with this step).

@@ -73,7 +73,7 @@ def gather(n_blocks=1024):
 def step(n=32, ctx=4096, reps=3):
     """A decode-only forward of the full Llama-3.1-8B (the CUDA-graph path):
     n sequences at ctx tokens of context."""
-    cfg = cs.model_config("llama8b", gpu_kv_capacity=24 << 30, host_kv_capacity=1 << 30, max_batched_tokens=8192,
+    cfg = cs.model_config("llama8b", gpu_kv_capacity=60 << 30, host_kv_capacity=1 << 30, max_batched_tokens=8192,
                           instrumented=0, max_entries=256)
     eng = cs.Engine(cfg)
     for r in range(n):
@@ -91,4 +91,5 @@ def step(n=32, ctx=4096, reps=3):
 
 
 if __name__ == "__main__":
-    {"decode": decode, "prefill": prefill, "gather": gather, "step": step}[sys.argv[1]]()
+    # optional integer arguments are passed through, e.g. `step 92 4130`
+    {"decode": decode, "prefill": prefill, "gather": gather, "step": step}[sys.argv[1]](*map(int, sys.argv[2:]))
