@@ -159,6 +159,8 @@ EXPORTS = {
     "cs_set_dry": ([E, C.c_int32], C.c_int),
     "cs_bench_attention": ([E, P(cs_batch_entry), C.c_int32, C.c_int32, P(C.c_double), P(C.c_int64),
                             P(C.c_int64)], C.c_int),
+    "cs_bench_gemm": ([E, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_double), P(C.c_double),
+                       P(C.c_double), P(C.c_double)], C.c_int),
     "cs_replay_run": ([E, P(C.c_int64), C.c_int64, C.c_int64, P(C.c_int64), P(C.c_double), P(C.c_double),
                        P(C.c_int32), P(C.c_double), P(C.c_int32), P(C.c_int64), P(C.c_int64),
                        P(cs_replay_stats)], C.c_int),

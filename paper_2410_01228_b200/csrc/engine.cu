@@ -14,6 +14,7 @@
 #include <time.h>
 
 #include <algorithm>
+#include <cmath>
 #include <array>
 #include <atomic>
 #include <condition_variable>
@@ -25,6 +26,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "../../include/conserve_b200.h"
@@ -57,6 +59,10 @@ bool launch_attention(const AttnParams& p, const CUtensorMap* kv_map, int head_d
                       int n_pt_grid, cudaStream_t s);
 int prefill_tile_rows();
 int prefill_tile_keys();
+int wgemm_stages(int Mp, size_t budget);
+bool wgemm_supported(int M, int N, int K);
+void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, int Mp, int N, int K, int splits,
+              int stages, bool f32_out, cudaStream_t s);
 void p2p_allreduce(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s);
 }  // namespace csk
 
@@ -252,6 +258,12 @@ struct cs_engine {
   std::map<int, bool> lt_tuned;
   void tune_gemms(int M);
   bool lt_gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
+  // K7 (csrc/gemm_tc.cu): the M <= 256 projections on our own tcgen05
+  // weight-streaming kernel; TMA maps per (tensor, rows, K, box rows)
+  bool use_wgemm = false;
+  std::map<std::tuple<const void*, int, int, int>, CUtensorMap> tmaps;
+  const CUtensorMap* tmap(const void* p, int rows, int K, int box_rows);
+  bool wgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
   ncclComm_t comm = nullptr;
   DescRing ring[2];
   double moved_ms[2] = {0, 0};
@@ -302,7 +314,7 @@ struct cs_engine {
     graphs.clear();
     ++graph_gen;
   }
-  void gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
+  int gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
   void allreduce(__nv_bfloat16* buf, int64_t count);
   // ---- peer-memory all-reduce: exchange region =
   // [2 partial buffers of (max_tok*hidden + 64) bf16][flag u64][step u64][arrive i32]
@@ -392,7 +404,16 @@ void validate(const cs_config& c) {
 // (block, layer, K|V, head) = 16 consecutive rows): 64-column x 16-row boxes,
 // SWIZZLE_128B to match the UMMA operand layout (attn_tc.cu). The driver entry
 // point is resolved through the runtime, so no -lcuda.
+// 2D bf16 tensor map over [rows][cols] (row-major), SWIZZLE_128B, box
+// 64 columns x box_rows rows; false when the driver rejects the shape.
+bool make_2d_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+
 void make_kv_tensor_map(CUtensorMap* map, void* pool, uint64_t rows, int D) {
+  if (rows >= (1ull << 31)) throw ConfigError("KV pool too large for 32-bit TMA row coordinates");
+  if (!make_2d_map(map, pool, rows, static_cast<uint64_t>(D), 16)) throw CudaError("cuTensorMapEncodeTiled failed");
+}
+
+bool make_2d_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -404,15 +425,14 @@ void make_kv_tensor_map(CUtensorMap* map, void* pool, uint64_t rows, int D) {
     if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
     encode = reinterpret_cast<EncodeFn>(fn);
   }
-  if (rows >= (1ull << 31)) throw ConfigError("KV pool too large for 32-bit TMA row coordinates");
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), rows};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
-  const cuuint32_t box[2] = {64, 16};
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), rows};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+  const cuuint32_t box[2] = {64, box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, pool, dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return r == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -515,12 +535,42 @@ void cs_engine::tune_gemms(int M) {
   CK(cudaGetLastError());
 }
 
-void cs_engine::gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32) {
-  if (M <= 0) return;
-  if (lt_gemm(A, W, C, M, N, K, out_f32)) return;
+const CUtensorMap* cs_engine::tmap(const void* p, int rows, int K, int box_rows) {
+  const auto key = std::make_tuple(p, rows, K, box_rows);
+  auto f = tmaps.find(key);
+  if (f != tmaps.end()) return &f->second;
+  CUtensorMap m;
+  if (!make_2d_map(&m, p, static_cast<uint64_t>(rows), static_cast<uint64_t>(K), static_cast<uint32_t>(box_rows)))
+    return nullptr;
+  return &tmaps.emplace(key, m).first->second;
+}
+
+bool cs_engine::wgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32) {
+  if (!use_wgemm || !csk::wgemm_supported(M, N, K)) return false;
+  const int Mp = (M + 15) / 16 * 16;
+  // X rows past M are out of the tensor: TMA fills them with zeros
+  const CUtensorMap* wm = tmap(W, N, K, 128);
+  const CUtensorMap* xm = tmap(A, M, K, Mp);
+  if (!wm || !xm) return false;
+  // one wave: >= one feature tile per SM -> two CTAs per SM, no split;
+  // fewer tiles -> one deep-ring CTA per SM and a K split (a cluster of <= 8)
+  const int n_tiles = N / 128;
+  const bool two = n_tiles >= sms;
+  const int stages = csk::wgemm_stages(Mp, two ? 112 * 1024 : 220 * 1024);
+  const int splits = two ? 1 : std::max(1, std::min({8, sms / n_tiles, K / 64 / 4}));
+  csk::wgemm_tc(wm, xm, C, M, Mp, N, K, splits, stages, out_f32, s_compute);
+  return true;
+}
+
+// Returns the number of hand-written kernels it launched (K7: 1, cuBLAS: 0).
+int cs_engine::gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32) {
+  if (M <= 0) return 0;
+  if (wgemm(A, W, C, M, N, K, out_f32)) return 1;
+  if (lt_gemm(A, W, C, M, N, K, out_f32)) return 0;
   const float alpha = 1.f, beta = 0.f;
   CKB(cublasGemmEx(blas, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, W, CUDA_R_16BF, K, A, CUDA_R_16BF, K, &beta, C,
                    out_f32 ? CUDA_R_32F : CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
+  return 0;
 }
 
 void cs_engine::allreduce(__nv_bfloat16* buf, int64_t count) {
@@ -595,7 +645,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
       }
     }
     csk::add_rmsnorm(x, l == 0 ? nullptr : tmp, w.attn_norm[l], xn, hidden, cfg.rms_eps, desc, nullptr, T, s_compute);
-    gemm(xn, w.wqkv[l], qkv, static_cast<int>(M), qkv_cols, hidden, false);
+    n_launch += gemm(xn, w.wqkv[l], qkv, static_cast<int>(M), qkv_cols, hidden, false);
     csk::rope_append(qkv, it.ap.tok_pos, it.d_tok_slot, kv, hq, hkv, D, L, l,
                      cfg.rope_theta, desc, T, s_compute);
     csk::AttnParams ap = it.ap;
@@ -604,16 +654,16 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
       throw ConfigError("unsupported attention shape");
     {
       __nv_bfloat16* part = partial_out(tmp);
-      gemm(attn, w.wo[l], part, static_cast<int>(M), hidden, hq * D, false);
+      n_launch += gemm(attn, w.wo[l], part, static_cast<int>(M), hidden, hq * D, false);
       if (part != tmp) ++n_launch;
       reduce_into(tmp, M * hidden);
     }
     csk::add_rmsnorm(x, tmp, w.mlp_norm[l], xn, hidden, cfg.rms_eps, desc, nullptr, T, s_compute);
-    gemm(xn, w.wgu[l], gu, static_cast<int>(M), 2 * ffn, hidden, false);
+    n_launch += gemm(xn, w.wgu[l], gu, static_cast<int>(M), 2 * ffn, hidden, false);
     csk::silu_mul(gu, act, ffn, desc, T, s_compute);
     {
       __nv_bfloat16* part = partial_out(tmp);
-      gemm(act, w.wd[l], part, static_cast<int>(M), hidden, ffn, false);
+      n_launch += gemm(act, w.wd[l], part, static_cast<int>(M), hidden, ffn, false);
       if (tp > 1) {
         if (part != tmp) ++n_launch;
         if (is_sp(l + 1)) {
@@ -637,7 +687,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   // Final norm of each entry's last row -> lm_head -> argmax.
   const int E = Eg;
   csk::add_rmsnorm(x, tmp, w.final_norm, xl, hidden, cfg.rms_eps, desc, it.d_ent_last, E, s_compute);
-  gemm(xl, w.lm_head, logits, E, vocab, hidden, true);
+  n_launch += gemm(xl, w.lm_head, logits, E, vocab, hidden, true);
   csk::argmax_rows(logits, vocab, reinterpret_cast<unsigned long long*>(d_out + sizeof(csk::IterDesc)), desc, E,
                    s_compute);
   CK(cudaMemcpyAsync(d_out, d_meta, sizeof(csk::IterDesc), cudaMemcpyDeviceToDevice, s_compute));
@@ -1140,6 +1190,10 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         CKB(cublasSetWorkspace(e->blas, e->blas_ws, 64u << 20));
         CKB(cublasSetMathMode(e->blas, CUBLAS_DEFAULT_MATH));
         CKB(cublasLtCreate(&e->lt));
+        {
+          const char* v = std::getenv("CS_WGEMM");  // K7 for the M <= 256 projections
+          e->use_wgemm = v && v[0] == '1';
+        }
         // Workspaces and the metadata buffer at their upper bounds, so no
         // iteration frees device memory (cudaFree synchronises the device:
         // it would stall the copy streams, and deadlock TP ranks that share
@@ -1554,6 +1608,58 @@ int cs_bench_attention(cs_engine* e, const cs_batch_entry* entries, int32_t n, i
     *flops = f;
     it.active = false;
     e->pool->on_forward_completed();
+  });
+}
+
+int cs_bench_gemm(cs_engine* e, int32_t M, int32_t N, int32_t K, int32_t reps, double* ms_k7, double* ms_cublas,
+                  double* max_abs_diff, double* max_abs_ref) {
+  return guard([&] {
+    if (e->host_only || e->no_model) throw std::logic_error("gemm bench needs a device engine");
+    if (!csk::wgemm_supported(M, N, K)) throw std::invalid_argument("gemm bench: M <= 256, N % 128, K % 64");
+    __nv_bfloat16 *x = nullptr, *w = nullptr, *y7 = nullptr, *yb = nullptr;
+    const size_t nx = static_cast<size_t>(M) * K, nw = static_cast<size_t>(N) * K, ny = static_cast<size_t>(M) * N;
+    CK(cudaMalloc(&x, nx * 2));
+    CK(cudaMalloc(&w, nw * 2));
+    CK(cudaMalloc(&y7, ny * 2));
+    CK(cudaMalloc(&yb, ny * 2));
+    csk::fill_pool(x, nx, 11, e->s_compute);
+    csk::fill_pool(w, nw, 12, e->s_compute);
+    const bool saved = e->use_wgemm;
+    auto time = [&](bool k7, __nv_bfloat16* y) {
+      e->use_wgemm = k7;
+      for (int r = 0; r < 3; ++r) e->gemm(x, w, y, M, N, K, false);
+      CK(cudaEventRecord(e->ev_start, e->s_compute));
+      for (int r = 0; r < reps; ++r) e->gemm(x, w, y, M, N, K, false);
+      CK(cudaEventRecord(e->ev_end, e->s_compute));
+      CK(cudaEventSynchronize(e->ev_end));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e->ev_start, e->ev_end));
+      return static_cast<double>(ms) / reps;
+    };
+    try {
+      *ms_k7 = time(true, y7);
+      *ms_cublas = time(false, yb);
+    } catch (...) {
+      e->use_wgemm = saved;
+      throw;
+    }
+    e->use_wgemm = saved;
+    CK(cudaGetLastError());
+    std::vector<__nv_bfloat16> h7(ny), hb(ny);
+    CK(cudaMemcpy(h7.data(), y7, ny * 2, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hb.data(), yb, ny * 2, cudaMemcpyDeviceToHost));
+    double md = 0, mr = 0;
+    for (size_t i = 0; i < ny; ++i) {
+      const double a = __bfloat162float(h7[i]), b = __bfloat162float(hb[i]);
+      md = std::max(md, std::fabs(a - b));
+      mr = std::max(mr, std::fabs(b));
+    }
+    *max_abs_diff = md;
+    *max_abs_ref = mr;
+    cudaFree(x);
+    cudaFree(w);
+    cudaFree(y7);
+    cudaFree(yb);
   });
 }
 

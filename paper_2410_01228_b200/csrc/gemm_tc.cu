@@ -1,0 +1,244 @@
+// K7: the decode-step projections (qkv, o_proj, gate|up, down, lm_head for
+// M <= 256 token rows) as a weight-streaming GEMM on the 5th-generation
+// tensor cores. At these M the GEMM is an HBM stream of the weights (436 MB
+// per Llama-3.1-8B layer) and cuBLAS leaves 20-55% of the bandwidth idle
+// (profiles/r1: o_proj 2.9 TB/s, down 3.9 TB/s at M = 128).
+//
+// Swap-AB: D[128 features, Mp tokens] = W_tile[128, K] . X[Mp, K]^T, so the
+// weight tile is the UMMA A operand (M = 128) and the few token rows are the
+// N dimension (Mp = M rounded up to 16, <= 256); both operands K-major,
+// 128-B swizzled, loaded by TMA (64 K-elements per stage). One CTA = one
+// 128-feature tile x one K range; the K ranges of a feature tile form a
+// thread-block cluster (<= 8 CTAs) whose fp32 partials are reduced through
+// distributed shared memory -- no global workspace, no atomics, no second
+// kernel. Warp roles (128 threads): warp 0 TMA producer, warp 1 UMMA issuer
+// (one elected lane each, warp-wide loops), then all four warps drain TMEM
+// (warp w owns lanes / features 32w .. 32w+31).
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace csk {
+
+namespace {
+
+constexpr int kFeat = 128;        // UMMA M: output features per CTA
+constexpr int kKc = 64;           // K elements per stage (one 128-B swizzled row)
+constexpr int kWBytes = kFeat * kKc * 2;  // 16 KB weight tile per stage
+constexpr int kGemmThreads = 128;
+constexpr int kMaxStages = 8;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cta address of this CTA -> the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_peer(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
+}  // namespace
+
+struct WgemmArgs {
+  void* y;            // [M, N] bf16 (or fp32 when f32_out)
+  int32_t M, Mp, N, K;
+  int32_t splits;     // cluster size along K (1..8) = gridDim.y
+  int32_t chunks;     // 64-element K chunks per split
+  int32_t f32_out;
+  int32_t stages;     // smem ring depth (<= kMaxStages)
+};
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    wgemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap xmap,
+                    WgemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int Mp = a.Mp;
+  const uint32_t stage_bytes = kWBytes + static_cast<uint32_t>(Mp) * 128;  // multiple of 2 KB
+  const int S = a.stages;
+  const uint32_t ring_bytes = S * stage_bytes;
+  const uint32_t red_bytes = static_cast<uint32_t>(Mp) * kFeat * 4;        // fp32 partial [Mp][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (ring_bytes > red_bytes ? ring_bytes : red_bytes));
+  uint64_t* full = bars;                 // [stages]
+  uint64_t* empty = bars + kMaxStages;   // [stages]
+  uint64_t* done = bars + 2 * kMaxStages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * kFeat;
+  const int split = blockIdx.y;
+  const int c_begin = split * a.chunks;
+  const int nc = min(a.chunks, a.K / kKc - c_begin);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    tc::mbar_init(done, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&wmap);
+    tc::prefetch_tmap(&xmap);
+  }
+  if (warp == 1) tc::tmem_alloc<256>(tslot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer --
+    for (int i = 0; i < nc; ++i) {
+      const int st = i % S;
+      if (i >= S) tc::mbar_wait(&empty[st], ((i / S) - 1) & 1);
+      if (tc::elect_one_sync()) {
+        uint8_t* sw = smem + st * stage_bytes;
+        const int kc = (c_begin + i) * kKc;
+        tc::mbar_expect_tx(&full[st], stage_bytes);
+        tc::tma_load_2d(sw, &wmap, &full[st], kc, n0);
+        tc::tma_load_2d(sw + kWBytes, &xmap, &full[st], kc, 0);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer --
+    const uint32_t idesc = tc::idesc_bf16_f32(kFeat, Mp, false, false);
+    const uint32_t base = tc::smem_u32(smem);
+    for (int i = 0; i < nc; ++i) {
+      const int st = i % S;
+      tc::mbar_wait(&full[st], (i / S) & 1);
+      tc::tc_fence_after();
+      if (tc::elect_one_sync()) {
+        const uint32_t wa = base + st * stage_bytes, xa = wa + kWBytes;
+#pragma unroll
+        for (int ks = 0; ks < kKc / 16; ++ks)
+          tc::umma_bf16_ss(tmem, tc::sdesc_sw128(wa + ks * 32, 16, 1024), tc::sdesc_sw128(xa + ks * 32, 16, 1024),
+                           idesc, (i > 0 || ks > 0) ? 1u : 0u);
+        tc::umma_commit(&empty[st]);
+        if (i == nc - 1) tc::umma_commit(done);
+      }
+      __syncwarp();
+    }
+  }
+
+  // ---------------------------------------------------------- epilogue --
+  // TMEM lane f = feature n0 + f, column c = token c. Partial -> own smem as
+  // red[c][f] (the ring is idle once `done` fired), cluster barrier, then CTA
+  // r of the cluster sums rows c = r, r + splits, ... over every peer's red
+  // and writes them (16-B stores along the features).
+  tc::mbar_wait(done, 0);
+  tc::tc_fence_after();
+  float* red = reinterpret_cast<float*>(smem);
+  const int f = warp * 32 + lane;
+  const uint32_t tl = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  for (int c0 = 0; c0 < Mp; c0 += 32) {
+    float v[32];
+    tc::tmem_ld32(tl + c0, v);
+    tc::tmem_wait_ld();
+    tc::reg_fence<32>(v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (c0 + i < Mp) red[(c0 + i) * kFeat + f] = v[i];
+  }
+  tc::tc_fence_before();
+  if (a.splits > 1) {
+    cluster_sync();
+  } else {
+    __syncthreads();
+  }
+  const uint32_t my_rank = a.splits > 1 ? cluster_rank() : 0;
+  const uint32_t red_s = tc::smem_u32(red);
+  // 32 threads per row (4 features each), 4 rows per pass
+  const int fq = (threadIdx.x & 31) * 4;
+  for (int c = static_cast<int>(my_rank) * 4 + (threadIdx.x >> 5); c < a.M; c += a.splits * 4) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint32_t off = static_cast<uint32_t>((c * kFeat + fq) * 4);
+    for (int q = 0; q < a.splits; ++q) {
+      const float4 t = a.splits > 1 ? ld_dsmem_f4(map_peer(red_s + off, q))
+                                    : *reinterpret_cast<const float4*>(red + c * kFeat + fq);
+      s.x += t.x;
+      s.y += t.y;
+      s.z += t.z;
+      s.w += t.w;
+    }
+    const size_t o = static_cast<size_t>(c) * a.N + n0 + fq;
+    if (a.f32_out) {
+      *reinterpret_cast<float4*>(static_cast<float*>(a.y) + o) = s;
+    } else {
+      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.y) + o) = make_uint2(pack_bf16(s.x, s.y), pack_bf16(s.z, s.w));
+    }
+  }
+  if (a.splits > 1) cluster_sync();  // peers keep their smem until every reader is done
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 1) tc::tmem_dealloc<256>(tmem);
+}
+
+size_t wgemm_smem_bytes(int Mp, int stages) {
+  const size_t stage = kWBytes + static_cast<size_t>(Mp) * 128;
+  const size_t ring = stages * stage, red = static_cast<size_t>(Mp) * kFeat * 4;
+  return (ring > red ? ring : red) + 256 + 1024;
+}
+
+// Ring depth that fits `budget` bytes of shared memory (>= 2).
+int wgemm_stages(int Mp, size_t budget) {
+  const size_t stage = kWBytes + static_cast<size_t>(Mp) * 128;
+  int s = kMaxStages;
+  while (s > 2 && wgemm_smem_bytes(Mp, s) > budget) --s;
+  return s;
+}
+
+bool wgemm_supported(int M, int N, int K) { return M >= 1 && M <= 256 && N % kFeat == 0 && K % kKc == 0; }
+
+// Y[M, N] = X[M, K] . W[N, K]^T. wmap: W as [N rows][K] (box 64 x 128);
+// xmap: X as [rows][K] (box 64 x Mp). splits x chunks covers K / 64; the K
+// splits of a feature tile are one cluster.
+void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, int Mp, int N, int K, int splits,
+              int stages, bool f32_out, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(wgemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  WgemmArgs a{};
+  a.y = y;
+  a.M = M;
+  a.Mp = Mp;
+  a.N = N;
+  a.K = K;
+  const int total = K / kKc;
+  a.chunks = (total + splits - 1) / splits;
+  a.splits = (total + a.chunks - 1) / a.chunks;
+  a.f32_out = f32_out ? 1 : 0;
+  a.stages = stages;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(N / kFeat, a.splits, 1);
+  cfg.blockDim = dim3(kGemmThreads, 1, 1);
+  cfg.dynamicSmemBytes = wgemm_smem_bytes(Mp, stages);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = a.splits;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, wgemm_tc_kernel, *wmap, *xmap, a);
+}
+
+}  // namespace csk
