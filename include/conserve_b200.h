@@ -267,7 +267,8 @@ int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin, int64_t op
 int cs_bench_attention(cs_engine* e, const cs_batch_entry* entries, int32_t n, int32_t reps, double* ms_per_launch,
                        int64_t* bytes, int64_t* flops);
 /* Times one M x N x K projection (Y = X W^T, bf16, seeded synthetic X and W)
- * on the engine's own tcgen05 weight-streaming kernel (K7) and on cuBLASLt:
+ * on the engine's own tcgen05 weight-streaming kernel (K7) and on cuBLASLt,
+ * rotating over copies of W that exceed the L2 (each launch reads W from HBM):
  * ms per launch of each, and the max |K7 - cuBLAS| / max |cuBLAS| of the
  * outputs. M <= 256, N % 128 == 0, K % 64 == 0. */
 int cs_bench_gemm(cs_engine* e, int32_t M, int32_t N, int32_t K, int32_t reps, double* ms_k7, double* ms_cublas,

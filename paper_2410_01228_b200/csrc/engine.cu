@@ -18,9 +18,11 @@
 #include <array>
 #include <atomic>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -60,6 +62,7 @@ bool launch_attention(const AttnParams& p, const CUtensorMap* kv_map, int head_d
 int prefill_tile_rows();
 int prefill_tile_keys();
 int wgemm_stages(int Mp, size_t budget);
+int wgemm_max_clusters(int Mp, int stages, int splits);
 bool wgemm_supported(int M, int N, int K);
 void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, int Mp, int N, int K, int splits,
               int stages, bool f32_out, cudaStream_t s);
@@ -260,10 +263,14 @@ struct cs_engine {
   bool lt_gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
   // K7 (csrc/gemm_tc.cu): the M <= 256 projections on our own tcgen05
   // weight-streaming kernel; TMA maps per (tensor, rows, K, box rows)
-  bool use_wgemm = false;
+  // 0 never (default: cuBLAS wins the decode step, profiles/r1/k7_gemm.md), 1 always for M <= 256
+  // (CS_WGEMM=1), 2 where tune_gemms timed it faster than the best cuBLAS plan (CS_WGEMM=2)
+  int wgemm_mode = 0;
+  std::map<uint64_t, bool> k7_pick;
   std::map<std::tuple<const void*, int, int, int>, CUtensorMap> tmaps;
   const CUtensorMap* tmap(const void* p, int rows, int K, int box_rows);
   bool wgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
+  bool wgemm_launch(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
   ncclComm_t comm = nullptr;
   DescRing ring[2];
   double moved_ms[2] = {0, 0};
@@ -456,28 +463,53 @@ bool cs_engine::lt_gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C,
 }
 
 // Times every heuristic candidate (up to 16) of the step's GEMM shapes at M
-// rows on the live weights and activation buffers (outputs land in buffers
-// the coming forward overwrites) and keeps the fastest; once per bucket,
-// before its graph is captured.
+// rows -- and K7, our tcgen05 weight-streaming kernel -- on the live weights
+// and activation buffers (outputs land in buffers the coming forward
+// overwrites) and keeps the fastest; once per bucket, before its graph is
+// captured. Each candidate runs over every layer's weight in turn, so the
+// weights stream from HBM as in a decode step (one layer's set would sit in
+// the 126 MB L2 and favour a different kernel).
 void cs_engine::tune_gemms(int M) {
   if (lt_tuned[M]) return;
   lt_tuned[M] = true;
   if (!lt) CKB(cublasLtCreate(&lt));
   struct Shape {
-    const __nv_bfloat16 *A, *W;
+    const __nv_bfloat16* A;
+    std::vector<const __nv_bfloat16*> W;
     void* C;
     int N, K;
     bool f32;
   };
   const int qkv_cols = (hq + 2 * hkv) * D;
-  const Shape shapes[] = {{xn, w.wqkv[0], qkv, qkv_cols, hidden, false},
-                          {attn, w.wo[0], tmp, hidden, hq * D, false},
-                          {xn, w.wgu[0], gu, 2 * ffn, hidden, false},
-                          {act, w.wd[0], tmp, hidden, ffn, false},
-                          {xl, w.lm_head, logits, vocab, hidden, true}};
+  std::vector<Shape> shapes(5);
+  shapes[0] = {xn, {}, qkv, qkv_cols, hidden, false};
+  shapes[1] = {attn, {}, tmp, hidden, hq * D, false};
+  shapes[2] = {xn, {}, gu, 2 * ffn, hidden, false};
+  shapes[3] = {act, {}, tmp, hidden, ffn, false};
+  shapes[4] = {xl, {w.lm_head}, logits, vocab, hidden, true};
+  for (int l = 0; l < L; ++l) {
+    shapes[0].W.push_back(w.wqkv[l]);
+    shapes[1].W.push_back(w.wo[l]);
+    shapes[2].W.push_back(w.wgu[l]);
+    shapes[3].W.push_back(w.wd[l]);
+  }
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
+  const float alpha = 1.f, beta = 0.f;
+  const size_t wsz = 64u << 20;
+  // ms per launch of `run` over every weight of the shape (after one warm pass)
+  auto time_over = [&](const Shape& sh, const std::function<bool(const __nv_bfloat16*)>& run) {
+    for (const __nv_bfloat16* W : sh.W)
+      if (!run(W)) return 1e30f;
+    CK(cudaEventRecord(e0, s_compute));
+    for (const __nv_bfloat16* W : sh.W) run(W);
+    CK(cudaEventRecord(e1, s_compute));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    return ms / static_cast<float>(sh.W.size());
+  };
   for (const Shape& sh : shapes) {
     if (sh.f32 && M > max_ent) continue;
     LtPlan pl;
@@ -491,7 +523,6 @@ void cs_engine::tune_gemms(int M) {
     CKB(cublasLtMatrixLayoutCreate(&pl.c, sh.f32 ? CUDA_R_32F : CUDA_R_16BF, sh.N, M, sh.N));
     cublasLtMatmulPreference_t pref;
     CKB(cublasLtMatmulPreferenceCreate(&pref));
-    const size_t wsz = 64u << 20;
     CKB(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsz, sizeof(wsz)));
     cublasLtMatmulHeuristicResult_t res[16];
     int n = 0;
@@ -499,22 +530,12 @@ void cs_engine::tune_gemms(int M) {
     cublasLtMatmulPreferenceDestroy(pref);
     float best = 1e30f;
     int bi = -1;
-    const float alpha = 1.f, beta = 0.f;
     for (int i = 0; hs == CUBLAS_STATUS_SUCCESS && i < n; ++i) {
       if (res[i].state != CUBLAS_STATUS_SUCCESS) continue;
-      bool ok = true;
-      for (int rep = 0; rep < 2 && ok; ++rep)  // warm-up
-        ok = cublasLtMatmul(lt, pl.op, &alpha, sh.W, pl.a, sh.A, pl.b, &beta, sh.C, pl.c, sh.C, pl.c, &res[i].algo,
-                            blas_ws, wsz, s_compute) == CUBLAS_STATUS_SUCCESS;
-      if (!ok) continue;
-      CK(cudaEventRecord(e0, s_compute));
-      for (int rep = 0; rep < 5; ++rep)
-        cublasLtMatmul(lt, pl.op, &alpha, sh.W, pl.a, sh.A, pl.b, &beta, sh.C, pl.c, sh.C, pl.c, &res[i].algo,
-                       blas_ws, wsz, s_compute);
-      CK(cudaEventRecord(e1, s_compute));
-      CK(cudaEventSynchronize(e1));
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, e0, e1));
+      const float ms = time_over(sh, [&](const __nv_bfloat16* W) {
+        return cublasLtMatmul(lt, pl.op, &alpha, W, pl.a, sh.A, pl.b, &beta, sh.C, pl.c, sh.C, pl.c, &res[i].algo,
+                              blas_ws, wsz, s_compute) == CUBLAS_STATUS_SUCCESS;
+      });
       if (ms < best) {
         best = ms;
         bi = i;
@@ -528,6 +549,17 @@ void cs_engine::tune_gemms(int M) {
       cublasLtMatrixLayoutDestroy(pl.a);
       cublasLtMatrixLayoutDestroy(pl.b);
       cublasLtMatrixLayoutDestroy(pl.c);
+    }
+    // K7 against the best cuBLAS plan (CS_WGEMM=2)
+    if (wgemm_mode == 2 && csk::wgemm_supported(M, sh.N, sh.K)) {
+      const float ms7 = time_over(sh, [&](const __nv_bfloat16* W) {
+        return wgemm_launch(sh.A, W, sh.C, M, sh.N, sh.K, sh.f32);
+      });
+      k7_pick[lt_key(M, sh.N, sh.K, sh.f32)] = ms7 < best;
+      static const bool verbose = std::getenv("CS_WGEMM_VERBOSE") != nullptr;
+      if (verbose)
+        std::fprintf(stderr, "tune M=%d N=%d K=%d: cuBLAS %.4f ms, K7 %.4f ms -> %s\n", M, sh.N, sh.K, best, ms7,
+                     ms7 < best ? "K7" : "cuBLAS");
     }
   }
   cudaEventDestroy(e0);
@@ -546,7 +578,17 @@ const CUtensorMap* cs_engine::tmap(const void* p, int rows, int K, int box_rows)
 }
 
 bool cs_engine::wgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32) {
-  if (!use_wgemm || !csk::wgemm_supported(M, N, K)) return false;
+  if (wgemm_mode == 0) return false;
+  if (wgemm_mode == 2) {  // tuned: only where it beat cuBLAS at this bucket
+    auto f = k7_pick.find(lt_key(M, N, K, out_f32));
+    if (f == k7_pick.end() || !f->second) return false;
+  }
+  return wgemm_launch(A, W, C, M, N, K, out_f32);
+}
+
+bool cs_engine::wgemm_launch(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K,
+                             bool out_f32) {
+  if (!csk::wgemm_supported(M, N, K)) return false;
   const int Mp = (M + 15) / 16 * 16;
   // X rows past M are out of the tensor: TMA fills them with zeros
   const CUtensorMap* wm = tmap(W, N, K, 128);
@@ -557,7 +599,21 @@ bool cs_engine::wgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, i
   const int n_tiles = N / 128;
   const bool two = n_tiles >= sms;
   const int stages = csk::wgemm_stages(Mp, two ? 112 * 1024 : 220 * 1024);
-  const int splits = two ? 1 : std::max(1, std::min({8, sms / n_tiles, K / 64 / 4}));
+  int splits = 1;
+  if (!two) {
+    // the largest power-of-two K split whose clusters all fit at once
+    static std::map<std::pair<int, int>, int> fit;  // (Mp, splits) -> resident clusters
+    for (int sp = 8; sp >= 2; sp /= 2) {
+      if (n_tiles * sp > 2 * sms || K / 64 / sp < 4) continue;
+      auto key = std::make_pair(Mp, sp);
+      auto f = fit.find(key);
+      if (f == fit.end()) f = fit.emplace(key, csk::wgemm_max_clusters(Mp, stages, sp)).first;
+      if (f->second >= n_tiles) {
+        splits = sp;
+        break;
+      }
+    }
+  }
   csk::wgemm_tc(wm, xm, C, M, Mp, N, K, splits, stages, out_f32, s_compute);
   return true;
 }
@@ -1192,7 +1248,7 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         CKB(cublasLtCreate(&e->lt));
         {
           const char* v = std::getenv("CS_WGEMM");  // K7 for the M <= 256 projections
-          e->use_wgemm = v && v[0] == '1';
+          e->wgemm_mode = (v && v[0] == '1') ? 1 : (v && v[0] == '2') ? 2 : 0;
         }
         // Workspaces and the metadata buffer at their upper bounds, so no
         // iteration frees device memory (cudaFree synchronises the device:
@@ -1618,18 +1674,21 @@ int cs_bench_gemm(cs_engine* e, int32_t M, int32_t N, int32_t K, int32_t reps, d
     if (!csk::wgemm_supported(M, N, K)) throw std::invalid_argument("gemm bench: M <= 256, N % 128, K % 64");
     __nv_bfloat16 *x = nullptr, *w = nullptr, *y7 = nullptr, *yb = nullptr;
     const size_t nx = static_cast<size_t>(M) * K, nw = static_cast<size_t>(N) * K, ny = static_cast<size_t>(M) * N;
+    // rotate over copies of W totalling >= 256 MB: every launch streams its
+    // weights from HBM, as in a decode step (the L2 holds 126 MB)
+    const int copies = static_cast<int>(std::max<size_t>(1, ((256u << 20) + nw * 2 - 1) / (nw * 2)));
     CK(cudaMalloc(&x, nx * 2));
-    CK(cudaMalloc(&w, nw * 2));
+    CK(cudaMalloc(&w, nw * 2 * copies));
     CK(cudaMalloc(&y7, ny * 2));
     CK(cudaMalloc(&yb, ny * 2));
     csk::fill_pool(x, nx, 11, e->s_compute);
-    csk::fill_pool(w, nw, 12, e->s_compute);
-    const bool saved = e->use_wgemm;
+    for (int c = 0; c < copies; ++c) csk::fill_pool(w + nw * c, nw, 12, e->s_compute);
+    const int saved = e->wgemm_mode;
     auto time = [&](bool k7, __nv_bfloat16* y) {
-      e->use_wgemm = k7;
-      for (int r = 0; r < 3; ++r) e->gemm(x, w, y, M, N, K, false);
+      e->wgemm_mode = k7 ? 1 : 0;
+      for (int r = 0; r < 3; ++r) e->gemm(x, w + nw * (r % copies), y, M, N, K, false);
       CK(cudaEventRecord(e->ev_start, e->s_compute));
-      for (int r = 0; r < reps; ++r) e->gemm(x, w, y, M, N, K, false);
+      for (int r = 0; r < reps; ++r) e->gemm(x, w + nw * (r % copies), y, M, N, K, false);
       CK(cudaEventRecord(e->ev_end, e->s_compute));
       CK(cudaEventSynchronize(e->ev_end));
       float ms = 0;
@@ -1640,10 +1699,10 @@ int cs_bench_gemm(cs_engine* e, int32_t M, int32_t N, int32_t K, int32_t reps, d
       *ms_k7 = time(true, y7);
       *ms_cublas = time(false, yb);
     } catch (...) {
-      e->use_wgemm = saved;
+      e->wgemm_mode = saved;
       throw;
     }
-    e->use_wgemm = saved;
+    e->wgemm_mode = saved;
     CK(cudaGetLastError());
     std::vector<__nv_bfloat16> h7(ny), hb(ny);
     CK(cudaMemcpy(h7.data(), y7, ny * 2, cudaMemcpyDeviceToHost));

@@ -241,4 +241,30 @@ void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, 
   cudaLaunchKernelEx(&cfg, wgemm_tc_kernel, *wmap, *xmap, a);
 }
 
+// Clusters of `splits` CTAs (each `smem` bytes) that can be resident at once.
+int wgemm_max_clusters(int Mp, int stages, int splits) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(wgemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1, splits, 1);
+  cfg.blockDim = dim3(kGemmThreads, 1, 1);
+  cfg.dynamicSmemBytes = wgemm_smem_bytes(Mp, stages);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = splits;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, wgemm_tc_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 }  // namespace csk

@@ -40,11 +40,11 @@ def test_k7_matches_cublas(eng, M, N, K):
 def test_forward_with_k7_matches_oracle(monkeypatch):
     monkeypatch.setenv("CS_WGEMM", "1")
     drv = Driver(cs.model_config("tiny", num_layers=2, hidden=512, n_heads=8, n_kv_heads=4, head_dim=64, ffn=1024,
-                                 vocab=1024))
+                                 vocab=1024, max_batched_tokens=1024))
     agree, rows = 0, 0
     try:
         for r in range(8):
-            drv.add(r, 20 + 23 * r, online=r < 2)
+            drv.add(r, 12 + 9 * r, online=r < 2)
         plans = [[(r, None) for r in range(8)]] * 5
         for plan in plans:
             info, lg, ref = drv.step(plan)
