@@ -44,6 +44,7 @@ __device__ __forceinline__ void load_page_async(uint8_t* sK, uint8_t* sV, const 
 // ------------------------------------------------------------------- K1 ----
 template <int D, int G>
 __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
+  pdl_trigger();
   constexpr int KS = D / 16;
   constexpr int NTD = D / 8;
   constexpr int PB = kPage * D * 2;  // bytes per K (or V) page

@@ -7,6 +7,13 @@
 
 namespace csk {
 
+// Programmatic dependent launch: lets a kernel launched with the
+// programmatic-serialization attribute (K7) start before this one finishes;
+// its griddepcontrol.wait still blocks until this grid completed and its
+// writes are visible. A no-op when no such dependent is queued.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Per-iteration counts. Written by the host (H2D) before the forward; the
 // safepoint kernel truncates the *_cur fields in place to the online prefix
 // when the preemption flag carries this iteration's epoch.

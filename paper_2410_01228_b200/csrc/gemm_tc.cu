@@ -101,16 +101,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc::tc_fence_after();
   const uint32_t tmem = *tslot;
 
+  const int rot = static_cast<int>(blockIdx.x) % max(nc, 1);
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer --
+    // The weights do not depend on the previous kernel: the first ring's
+    // worth is requested before griddepcontrol.wait (PDL launch), the
+    // activations only after it.
+    const int pre = min(S, nc);
+    if (tc::elect_one_sync()) {
+      for (int i = 0; i < pre; ++i) {
+        const int kc = (c_begin + (i + rot) % nc) * kKc;
+        tc::mbar_expect_tx(&full[i], stage_bytes);
+        tc::tma_load_2d(smem + i * stage_bytes, &wmap, &full[i], kc, n0);
+      }
+    }
+    __syncwarp();
+    pdl_wait();
     for (int i = 0; i < nc; ++i) {
       const int st = i % S;
       if (i >= S) tc::mbar_wait(&empty[st], ((i / S) - 1) & 1);
       if (tc::elect_one_sync()) {
         uint8_t* sw = smem + st * stage_bytes;
-        const int kc = (c_begin + i) * kKc;
-        tc::mbar_expect_tx(&full[st], stage_bytes);
-        tc::tma_load_2d(sw, &wmap, &full[st], kc, n0);
+        // feature tiles start their K loop at different chunks: the X tile
+        // every CTA of a split needs is not fetched by all of them at once
+        const int kc = (c_begin + (i + rot) % nc) * kKc;
+        if (i >= pre) {
+          tc::mbar_expect_tx(&full[st], stage_bytes);
+          tc::tma_load_2d(sw, &wmap, &full[st], kc, n0);
+        }
         tc::tma_load_2d(sw + kWBytes, &xmap, &full[st], kc, 0);
       }
       __syncwarp();
@@ -143,6 +161,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // and writes them (16-B stores along the features).
   tc::mbar_wait(done, 0);
   tc::tc_fence_after();
+  pdl_wait();  // (returns at once: the producer's wait already saw the previous grid complete)
   float* red = reinterpret_cast<float*>(smem);
   const int f = warp * 32 + lane;
   const uint32_t tl = tmem + (static_cast<uint32_t>(warp * 32) << 16);
@@ -231,13 +250,15 @@ void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, 
   cfg.blockDim = dim3(kGemmThreads, 1, 1);
   cfg.dynamicSmemBytes = wgemm_smem_bytes(Mp, stages);
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 1;
   at[0].val.clusterDim.y = a.splits;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: see the producer
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, wgemm_tc_kernel, *wmap, *xmap, a);
 }
 

@@ -60,6 +60,7 @@ template <int CH>
 __global__ void add_rmsnorm_kernel(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16* w,
                                    __nv_bfloat16* xn, int hidden, float eps, const IterDesc* desc,
                                    const int32_t* row_idx) {
+  pdl_trigger();  // the next projection (K7) may start streaming its weights
   const int i = blockIdx.x;
   int r;
   if (row_idx != nullptr) {
@@ -141,6 +142,7 @@ void add_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16
 
 // ----------------------------------------------------------------- SwiGLU ----
 __global__ void silu_mul_kernel(const __nv_bfloat16* gu, __nv_bfloat16* act, int ffn, const IterDesc* desc) {
+  pdl_trigger();
   const int t = blockIdx.y;
   if (t >= desc->n_tok_cur) return;
   const __nv_bfloat16* g = gu + static_cast<size_t>(t) * 2 * ffn;

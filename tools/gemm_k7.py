@@ -20,12 +20,13 @@ SHAPES = [  # (name, N, K)
     ("lm_head", 128256, 4096)]
 
 
-def main(reps=50):
+def main(reps=50, only=None):
     cfg = cs.model_config("llama8b", hidden=512, ffn=512, vocab=512, gpu_kv_capacity=1 << 30,
                           host_kv_capacity=1 << 28, max_batched_tokens=1024, instrumented=0)
     eng = cs.Engine(cfg)
-    for M in (8, 32, 64, 128, 256):
-        for name, N, K in SHAPES:
+    cases = [(M, s) for M in (8, 32, 64, 128, 256) for s in SHAPES] if only is None else [(only[0], ("one",) + only[1:])]
+    for M, (name, N, K) in cases:
+        if True:
             a, b, d, r = C.c_double(), C.c_double(), C.c_double(), C.c_double()
             cs.engine._check(cs.lib().cs_bench_gemm(eng._h, M, N, K, reps, C.byref(a), C.byref(b), C.byref(d),
                                                     C.byref(r)))
@@ -38,4 +39,6 @@ def main(reps=50):
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 50)
+    # python tools/gemm_k7.py [reps [M N K]]
+    a = [int(x) for x in sys.argv[1:]]
+    main(a[0] if a else 50, tuple(a[1:4]) if len(a) >= 4 else None)
