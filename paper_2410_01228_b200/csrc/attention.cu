@@ -276,11 +276,7 @@ static void launch_attention_t(const AttnParams& p, const CUtensorMap* kv_map, i
                                cudaStream_t s) {
   if (n_dec_grid > 0) {
     const int smem = decode_smem_bytes(D);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(attn_decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr = true;
-    }
+    smem_attr_once(reinterpret_cast<const void*>(attn_decode_kernel<D, G>), smem);
     dim3 grid(p.n_splits, p.hkv, n_dec_grid);
     attn_decode_kernel<D, G><<<grid, 128, smem, s>>>(p);
   }

@@ -487,12 +487,7 @@ __global__ void __launch_bounds__(256) attn_prefill_combine_kernel(AttnParams p)
 
 template <int D, int G>
 void launch_prefill_tc_t(const AttnParams& p, const CUtensorMap* kv_map, int n_pt_grid, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_prefill_tc_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         TcLayout<D>::launch_bytes);
-    attr = true;
-  }
+  smem_attr_once(reinterpret_cast<const void*>(attn_prefill_tc_kernel<D, G>), TcLayout<D>::launch_bytes);
   attn_prefill_tc_kernel<D, G><<<dim3(n_pt_grid * p.hkv, 1, p.k2_splits), kThreads, TcLayout<D>::launch_bytes, s>>>(
       p, *kv_map);
   if (p.k2_splits > 1) attn_prefill_combine_kernel<D, G><<<dim3(n_pt_grid, p.hkv, D / 32), 256, 0, s>>>(p);

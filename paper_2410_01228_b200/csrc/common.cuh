@@ -5,7 +5,26 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 namespace csk {
+
+// Opt a kernel into `bytes` of dynamic shared memory on the current device.
+// The attribute is per device, so it is remembered per (kernel, device): one
+// process may drive several GPUs (or several engines share one).
+inline void smem_attr_once(const void* fn, int bytes) {
+  static std::mutex m;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(m);
+  int& have = done[std::make_pair(fn, dev)];
+  if (have >= bytes) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  have = bytes;
+}
 
 // Programmatic dependent launch: lets a kernel launched with the
 // programmatic-serialization attribute (K7) start before this one finishes;

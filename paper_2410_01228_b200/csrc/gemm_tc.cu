@@ -229,11 +229,7 @@ bool wgemm_supported(int M, int N, int K) { return M >= 1 && M <= 256 && N % kFe
 // splits of a feature tile are one cluster.
 void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, int Mp, int N, int K, int splits,
               int stages, bool f32_out, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(wgemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  smem_attr_once(reinterpret_cast<const void*>(wgemm_tc_kernel), 227 * 1024);
   WgemmArgs a{};
   a.y = y;
   a.M = M;
@@ -264,11 +260,7 @@ void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, 
 
 // Clusters of `splits` CTAs (each `smem` bytes) that can be resident at once.
 int wgemm_max_clusters(int Mp, int stages, int splits) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(wgemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  smem_attr_once(reinterpret_cast<const void*>(wgemm_tc_kernel), 227 * 1024);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(1, splits, 1);
   cfg.blockDim = dim3(kGemmThreads, 1, 1);
