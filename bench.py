@@ -336,13 +336,18 @@ def run_reference(args):
     g = os.path.join(ROOT, "tests", "golden", name)
     tr = R.load(os.path.join(g, "calls.jsonl.gz"), os.path.join(g, "requests.jsonl.gz"))
     k = pick_cpu_iteration(tr)
+    # each step is a bounded (~8 s) CPU sample: at most 1 warm-up and 4 timed
+    # steps, so the arm finishes in about a minute whatever --steps asks for
+    warm = max(0, min(args.warmup, 1))
+    for _ in range(warm):
+        cpu_port_sample(tr, R, k)
     vals = []
-    for _ in range(max(1, min(args.steps, 2))):
+    for _ in range(max(1, min(args.steps, 4))):
         vals.append(cpu_port_sample(tr, R, k))
     v = float(np.median([x["value"] for x in vals]))
     base = vals[0]
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": len(vals), "warmup": 0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "steps": len(vals), "warmup": warm, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{name} co-serving trace (reference SimEngine decisions), CPU port sample"},
             "cpu_baseline": dict(base, value=v),
