@@ -144,7 +144,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_full = s_full + 2;                 // [query tile]
   uint64_t* o_done = p_full + 2;                 // [query tile] once per PV
   uint64_t* o_final = o_done + 2;                // [query tile] after the last PV
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 2);
+  uint64_t* q_ready = o_final + 2;               // [query tile] Q tile staged in smem
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_ready + 2);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
@@ -159,11 +160,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&o_done[i], 1);
       tc::mbar_init(&o_final[i], 1);
+      tc::mbar_init(&q_ready[i], kRows);
     }
     tc::fence_mbar_init();
   }
   if (warp == 8 && lane == 0) tc::prefetch_tmap(&kv_map);
   if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
 
   // Q tiles: softmax thread (i, r) loads packed row row0 + 128 i + r (token
   // q0 + gr/G, head kvh*G + gr%G) into the SWIZZLE_128B K-major UMMA layout.
@@ -183,11 +189,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     tc::fence_async_smem();
+    tc::mbar_arrive(&q_ready[qi]);  // the TMA warp is already streaming K/V meanwhile
   }
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
 
   if (warp == 8) {
     // ------------------------------------------------------ TMA producer --
@@ -278,7 +281,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       // prologue: S(0) for both query tiles
       wait_k(0);
-      for (int qi = 0; qi < nq; ++qi) issue_s(qi, 0);
+      for (int qi = 0; qi < nq; ++qi) {
+        tc::mbar_wait(&q_ready[qi], 0);
+        issue_s(qi, 0);
+      }
       // ping-pong: while softmax i makes P_i(j), the tensor core runs the
       // other tile's PV / S
       for (int j = 0; j < n_kt; ++j) {
