@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_prefill_tc_kernel(AttnParams p, const __grid_constant__ CUtensorMap kv_map) {
   using Lay = TcLayout<D>;
   constexpr int CH = Lay::kChunks;
+  const long long t_kernel = K2T_NOW();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // blockIdx.x = (rank of the tile in the heaviest-first order) x hkv + KV
@@ -450,6 +451,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::tc_fence_after();
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
+#ifdef CS_K2_TIMERS
+  if (threadIdx.x == 0 && kvh == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - p.hkv) && blockIdx.z == 0)
+    printf("K2T cta  cta=%d n_kt=%d kernel=%lld\n", blockIdx.x, n_kt, clock64() - t_kernel);
+#endif
+  (void)t_kernel;
 }
 
 // Split-K merge for K2: one CTA per (tile, KV head, 32 head dims), one thread
