@@ -423,8 +423,15 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         sampler.start()
+        # launch lists: `ncu --profile-from-start off` + CS_PROFILE_REGION=1
+        # record the timed region only (not start-up GEMM tuning)
+        prof = os.environ.get("CS_PROFILE_REGION") == "1" and name == main_trace
+        if prof:
+            torch.cuda.profiler.start()
         res = R.run(eng, tr, W, W + K)
         torch.cuda.synchronize()
+        if prof:
+            torch.cuda.profiler.stop()
         if dist:
             dist.barrier()
         clocks = sampler.stop()

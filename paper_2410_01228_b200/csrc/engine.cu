@@ -466,7 +466,7 @@ bool cs_engine::lt_gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C,
 // rows -- and K7, our tcgen05 weight-streaming kernel -- on the live weights
 // and activation buffers (outputs land in buffers the coming forward
 // overwrites) and keeps the fastest; once per bucket, before its graph is
-// captured. Each candidate runs over every layer's weight in turn, so the
+// captured. Each candidate runs over up to 8 layers' weights in turn, so the
 // weights stream from HBM as in a decode step (one layer's set would sit in
 // the 126 MB L2 and favour a different kernel).
 void cs_engine::tune_gemms(int M) {
@@ -487,7 +487,7 @@ void cs_engine::tune_gemms(int M) {
   shapes[2] = {xn, {}, gu, 2 * ffn, hidden, false};
   shapes[3] = {act, {}, tmp, hidden, ffn, false};
   shapes[4] = {xl, {w.lm_head}, logits, vocab, hidden, true};
-  for (int l = 0; l < L; ++l) {
+  for (int l = 0; l < std::min(L, 8); ++l) {  // 8 layers' weights exceed the L2 several times over
     shapes[0].W.push_back(w.wqkv[l]);
     shapes[1].W.push_back(w.wo[l]);
     shapes[2].W.push_back(w.wgu[l]);

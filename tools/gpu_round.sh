@@ -18,7 +18,7 @@ if has tests; then timeout 900 python -m pytest tests -m gpu -x -q > "$OUT/pytes
 if has bench; then timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/bench.err"; fi
 NCU="ncu --clock-control none"
 if has launches; then
-  CS_NO_PACING=1 timeout 1200 $NCU --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
+  CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
 fi
 if has k1; then
