@@ -555,7 +555,9 @@ def main():
                      "algorithmic_bytes": dec.get("bytes"),
                      "traffic_source": traffic.get("K1", {}).get("source"),
                      "peak_kind": peak_kind,
-                     "prefill_K2": probes.get("attention", {}).get("prefill")},
+                     "prefill_K2": dict(probes.get("attention", {}).get("prefill") or {}, bound="tensor",
+                                        unit="TFLOP/s", traffic=traffic.get("K2", {}).get("dram_bytes"),
+                                        traffic_source=traffic.get("K2", {}).get("source"))},
         "cpu_baseline": cpu,
         "clocks": clocks,
         "gpu_launches": int(s1.kernel_launches - s0.kernel_launches),
