@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <cstdio>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace csk {
@@ -406,8 +408,15 @@ void kv_move(bool to_host, __nv_bfloat16* pool, __nv_bfloat16* host_mapped, cons
              int runs_per_seg, int D, int sms, cudaStream_t s) {
   if (n_segs <= 0) return;
   const int64_t items = static_cast<int64_t>(n_segs) * runs_per_seg;
+  // The copy is host-link bound (~57 GB/s): a few CTAs per SM keep enough
+  // stores in flight, more only take thread slots from the concurrent forward.
+  static const int per_sm = [] {
+    const char* v = std::getenv("CS_KV_MOVE_CTAS_PER_SM");
+    const int n = v ? std::atoi(v) : 2;  // profiles/r1/SUMMARY.md (calls r2p, r2q)
+    return n < 1 ? 1 : n;
+  }();
   int64_t grid = (items + 7) / 8;
-  if (grid > sms * 8) grid = sms * 8;
+  if (grid > static_cast<int64_t>(sms) * per_sm) grid = static_cast<int64_t>(sms) * per_sm;
   if (grid < 1) grid = 1;
   const SegDesc* sd = static_cast<const SegDesc*>(segs_mapped);
   if (to_host) {
