@@ -1142,9 +1142,15 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
     if (!e->host_only) {
       CK(cudaSetDevice(cfg->device));
       CK(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, cfg->device));
-      CK(cudaStreamCreateWithFlags(&e->s_compute, cudaStreamNonBlocking));
-      CK(cudaStreamCreateWithFlags(&e->s_d2h, cudaStreamNonBlocking));
-      CK(cudaStreamCreateWithFlags(&e->s_h2d, cudaStreamNonBlocking));
+      // the forward gets the block scheduler first; the host-link-bound
+      // checkpoint / restore copies fill in behind it
+      int prio_low = 0, prio_high = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
+      const char* np = std::getenv("CS_NO_STREAM_PRIORITY");
+      if (np && np[0] == '1') prio_low = prio_high = 0;
+      CK(cudaStreamCreateWithPriority(&e->s_compute, cudaStreamNonBlocking, prio_high));
+      CK(cudaStreamCreateWithPriority(&e->s_d2h, cudaStreamNonBlocking, prio_low));
+      CK(cudaStreamCreateWithPriority(&e->s_h2d, cudaStreamNonBlocking, prio_low));
       CK(cudaEventCreate(&e->ev_start));
       CK(cudaEventCreate(&e->ev_end));
       CK(cudaEventCreateWithFlags(&e->ev_fwd_done, cudaEventDisableTiming));
