@@ -267,6 +267,7 @@ struct cs_engine {
   // (CS_WGEMM=1), 2 where tune_gemms timed it faster than the best cuBLAS plan (CS_WGEMM=2)
   int wgemm_mode = 0;
   std::map<uint64_t, bool> k7_pick;
+  std::map<std::pair<int, int>, int> k7_clusters;  // (Mp, K split) -> co-resident clusters (per engine: no shared state)
   std::map<std::tuple<const void*, int, int, int>, CUtensorMap> tmaps;
   const CUtensorMap* tmap(const void* p, int rows, int K, int box_rows);
   bool wgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
@@ -602,12 +603,11 @@ bool cs_engine::wgemm_launch(const __nv_bfloat16* A, const __nv_bfloat16* W, voi
   int splits = 1;
   if (!two) {
     // the largest power-of-two K split whose clusters all fit at once
-    static std::map<std::pair<int, int>, int> fit;  // (Mp, splits) -> resident clusters
     for (int sp = 8; sp >= 2; sp /= 2) {
       if (n_tiles * sp > 2 * sms || K / 64 / sp < 4) continue;
       auto key = std::make_pair(Mp, sp);
-      auto f = fit.find(key);
-      if (f == fit.end()) f = fit.emplace(key, csk::wgemm_max_clusters(Mp, stages, sp)).first;
+      auto f = k7_clusters.find(key);
+      if (f == k7_clusters.end()) f = k7_clusters.emplace(key, csk::wgemm_max_clusters(Mp, stages, sp)).first;
       if (f->second >= n_tiles) {
         splits = sp;
         break;
