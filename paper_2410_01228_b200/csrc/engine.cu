@@ -425,14 +425,14 @@ bool make_2d_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t col
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static EncodeFn encode = nullptr;
-  if (!encode) {
+  // resolved once (thread-safe static initialisation: engines may build maps concurrently)
+  static const EncodeFn encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q{};
     CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
     if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
-    encode = reinterpret_cast<EncodeFn>(fn);
-  }
+    return reinterpret_cast<EncodeFn>(fn);
+  }();
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), rows};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
   const cuuint32_t box[2] = {64, box_rows};
