@@ -1,0 +1,40 @@
+"""bench.py's JSON-line contract, checked on the CPU through the reference arm
+(`--impl reference`: the CPU port of the path on one bounded sample of the
+headline workload) and its helpers. The GPU arm prints the same keys plus
+roofline / clocks / gpu_launches; it runs on the B200 (driver, gpurun)."""
+import json
+import os
+import subprocess
+import sys
+
+from conftest import ROOT
+
+
+def test_reference_arm_prints_one_contract_line():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "higher_is_better", "scaling", "vs_baseline",
+              "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference"
+    assert d["value"] > 0 and d["higher_is_better"] is True
+    assert d["unit"] == "tok/s" and d["e2e"]["unit"] == "tok/s"
+    assert d["e2e"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    cb = d["cpu_baseline"]
+    assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == d["value"]
+    assert "workload" in d["config"] and cb["sample"]
+
+
+def test_percentile_is_nearest_rank():
+    sys.path.insert(0, ROOT)
+    import bench
+    xs = [5.0, 1.0, 4.0, 2.0, 3.0]
+    assert bench.percentile(xs, 0.99) == 5.0
+    assert bench.percentile(xs, 0.5) == 3.0
+    assert bench.percentile(xs, 0.2) == 1.0
+    assert bench.percentile([], 0.99) == 0.0
