@@ -151,3 +151,33 @@ def test_k2_split_k_small_chunks_over_long_context():
         _check_rows(eng, [e4], [list(range(4020, 4060))], 40)
     finally:
         eng.close()
+
+
+def test_k2_recompute_of_discarded_pages():
+    """Recompute entries (kv_cache.cpp:76-107, scheduler.cpp:286): every page of
+    an offline request is discarded, then re-materialised head-first in two
+    whole-page chunks (recompute_chunk, the last page partial); each chunk's
+    rows sit at the positions of its pages and attend causally over the
+    already re-materialised prefix. A decode after the recompute reads the
+    rebuilt KV."""
+    eng = _engine()
+    try:
+        eng.register_request(0, False)
+        _run(eng, [cs.BatchEntry(0, 700, 0, cs.CS_PREFILL, False)], [700])
+        st = eng.discard_request(0)
+        assert st.discarded_tokens == 700
+        done = 0
+        for cap in (320, 4096):
+            n = eng.recompute_chunk(0, 700 - done, cap)
+            assert n > 0 and (n % 16 == 0 or done + n == 700)
+            e = cs.BatchEntry(0, n, 700, cs.CS_RECOMPUTE, False)
+            _run(eng, [e], [n])
+            _check_rows(eng, [e], [list(range(done, done + n))], n)
+            done += n
+        assert done == 700 and eng.recompute_chunk(0, 1, 4096) == 0
+        dec = cs.BatchEntry(0, 1, 700, cs.CS_DECODE, False)
+        _run(eng, [dec], [1])
+        _check_rows(eng, [dec], [[699]], 1)
+        eng.audit()
+    finally:
+        eng.close()
