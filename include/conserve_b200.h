@@ -97,7 +97,7 @@ typedef struct cs_config {
   int64_t extra_blocks;          /* physical-pool slack over ceil(cap/page_bytes); <0 = auto */
   int64_t extra_host_slots;      /* host-pool slack; <0 = auto */
   int32_t max_entries;           /* max entries per plan (0 = 1024) */
-  int32_t layer_lookahead;       /* layers enqueued ahead of the device (0 = 2) */
+  int32_t layer_lookahead;       /* unused since r2 (the forward is no longer host-paced); kept for ABI */
   /* --- sharding (KV-head groups) --- */
   int32_t tp_rank;
   int32_t tp_size;
@@ -173,9 +173,20 @@ int cs_kv_prefetch_inflight(cs_engine* e, int64_t id, int32_t* out);
  * (kv_cache.cpp:428-455), H2D on its own stream. */
 int cs_kv_start_prefetch(cs_engine* e, int64_t id, int64_t now, cs_transfer_job* job, int32_t* has_job);
 int cs_kv_recompute_chunk(cs_engine* e, int64_t id, int64_t desired, int64_t cap, int64_t* out);
-/* Completion (kv_cache.cpp:471-520). Blocks until the real transfer's event
- * has completed, then applies the bookkeeping. */
+/* Completion (kv_cache.cpp:471-520; the reference engine calls it at the job's
+ * modelled done_time, sim_engine.cpp:242-248). Applies the bookkeeping without
+ * waiting for the device: blocks and host slots stay quarantined until the
+ * device jobs that touch them complete, a restore is stream-ordered after the
+ * gathers still writing its slots, and the next forward after the restores
+ * of the blocks it reads. Never blocks the caller. */
 int cs_kv_on_transfer_done(cs_engine* e, int64_t job_id, int64_t now, cs_transfer_done* out);
+/* Real completion of a transfer job (SURVEY.md 8b "Completion"): *done = 1
+ * once its device copy finished; *ms = the copy's device time (-1 while it
+ * runs, 0 if it moved nothing on the device). cs_job_wait blocks until done.
+ * Replaces the reference's modelled TransferChannel done_time in live mode
+ * (kv_cache.cpp:23-36). */
+int cs_job_poll(cs_engine* e, int64_t job_id, int32_t* done, double* ms);
+int cs_job_wait(cs_engine* e, int64_t job_id, double* ms);
 int cs_kv_on_request_paused(cs_engine* e, int64_t id, uint64_t pause_seq);
 int cs_kv_on_request_active(cs_engine* e, int64_t id);
 int cs_kv_release_request(cs_engine* e, int64_t id);

@@ -136,6 +136,8 @@ EXPORTS = {
     "cs_kv_start_prefetch": ([E, C.c_int64, C.c_int64, P(cs_transfer_job), P(C.c_int32)], C.c_int),
     "cs_kv_recompute_chunk": ([E, C.c_int64, C.c_int64, C.c_int64, P(C.c_int64)], C.c_int),
     "cs_kv_on_transfer_done": ([E, C.c_int64, C.c_int64, P(cs_transfer_done)], C.c_int),
+    "cs_job_poll": ([E, C.c_int64, P(C.c_int32), P(C.c_double)], C.c_int),
+    "cs_job_wait": ([E, C.c_int64, P(C.c_double)], C.c_int),
     "cs_kv_on_request_paused": ([E, C.c_int64, C.c_uint64], C.c_int),
     "cs_kv_on_request_active": ([E, C.c_int64], C.c_int),
     "cs_kv_release_request": ([E, C.c_int64], C.c_int),

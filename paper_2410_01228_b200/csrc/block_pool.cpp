@@ -45,6 +45,10 @@ BlockPool::BlockPool(const PoolConfig& cfg, Mover* mover) : cfg_(cfg), mover_(mo
   for (int64_t b = cfg.n_blocks; b-- > 0;) free_blocks_.push_back(static_cast<int32_t>(b));
   free_slots_.reserve(static_cast<size_t>(cfg.n_slots));
   for (int64_t s = cfg.n_slots; s-- > 0;) free_slots_.push_back(static_cast<int32_t>(s));
+  blk_d2h_.assign(static_cast<size_t>(cfg.n_blocks), 0);
+  blk_h2d_.assign(static_cast<size_t>(cfg.n_blocks), 0);
+  slot_d2h_.assign(static_cast<size_t>(cfg.n_slots), 0);
+  slot_h2d_.assign(static_cast<size_t>(cfg.n_slots), 0);
 }
 
 Req& BlockPool::req(int64_t id) {
@@ -89,37 +93,88 @@ int32_t BlockPool::take_slot() {
 
 void BlockPool::retire_block(Page& p) {
   if (p.block < 0) return;
-  block_q_.push_back({p.block, fwd_launched_, issued_[CS_D2H], issued_[CS_H2D]});
+  const size_t b = static_cast<size_t>(p.block);
+  block_q_.push_back({p.block, fwd_launched_, blk_d2h_[b], blk_h2d_[b]});
   p.last_block = p.block;
   p.block = -1;
 }
 
 void BlockPool::retire_slot(Page& p) {
   if (p.slot < 0) return;
-  slot_q_.push_back({p.slot, 0, issued_[CS_D2H], issued_[CS_H2D]});
+  const size_t s = static_cast<size_t>(p.slot);
+  slot_q_.push_back({p.slot, 0, slot_d2h_[s], slot_h2d_[s]});
   p.slot = -1;
 }
 
-bool BlockPool::job_prefix_done(int32_t dir, int64_t tag) const {
-  return done_prefix_[dir] >= tag;
+// True once device job `ord` of `dir` has completed (no device: always).
+bool BlockPool::dev_done(int32_t dir, int64_t ord) {
+  if (ord <= dev_done_[dir]) return true;
+  if (mover_ == nullptr) return true;
+  dev_done_[dir] = mover_->done_prefix(dir);
+  return ord <= dev_done_[dir];
+}
+
+// One device gather / restore; records it as the last job touching each
+// block and slot of its segments. A gather first waits for restores still
+// writing its blocks; a restore for gathers still writing its slots (a page
+// whose last delta is still in flight can be evicted and restored at once:
+// ADVICE r1, restore ordering).
+int64_t BlockPool::launch_gather(const std::vector<Segment>& segs) {
+  if (mover_ == nullptr || segs.empty()) return 0;
+  int64_t after = 0;
+  for (const Segment& g : segs) after = std::max(after, blk_h2d_[static_cast<size_t>(g.block)]);
+  if (dev_done(CS_H2D, after)) after = 0;
+  const int64_t ord = mover_->gather_to_host(segs, after);
+  if (ord > 0) {
+    for (const Segment& g : segs) {
+      blk_d2h_[static_cast<size_t>(g.block)] = ord;
+      slot_d2h_[static_cast<size_t>(g.slot)] = ord;
+    }
+  }
+  return ord;
+}
+
+int64_t BlockPool::launch_scatter(const std::vector<Segment>& segs) {
+  if (mover_ == nullptr || segs.empty()) return 0;
+  int64_t after = 0;
+  for (const Segment& g : segs) after = std::max(after, slot_d2h_[static_cast<size_t>(g.slot)]);
+  if (dev_done(CS_D2H, after)) after = 0;
+  const int64_t ord = mover_->scatter_from_host(segs, after);
+  if (ord > 0) {
+    for (const Segment& g : segs) {
+      blk_h2d_[static_cast<size_t>(g.block)] = ord;
+      slot_h2d_[static_cast<size_t>(g.slot)] = ord;
+    }
+  }
+  return ord;
 }
 
 // A freed block is reusable once (a) the forward dispatched after its release
 // has completed -- so a plan that still reads it (reference defect D3) reads
-// stale-but-intact KV -- and (b) every transfer issued before the release has
-// completed (a gather may still be reading it, a restore may be writing it).
+// stale-but-intact KV -- and (b) the last device gather reading it and the
+// last restore writing it have completed. Slots likewise wait only for the
+// device jobs that touched them (no hold behind unrelated copies).
 void BlockPool::reclaim() {
   auto keep_b = std::stable_partition(block_q_.begin(), block_q_.end(), [&](const Quarantined& q) {
-    return !((!cfg_.fwd_quarantine || fwd_completed_ >= q.fwd_tag + 1) && job_prefix_done(CS_D2H, q.d2h_tag) &&
-             job_prefix_done(CS_H2D, q.h2d_tag));
+    return !((!cfg_.fwd_quarantine || fwd_completed_ >= q.fwd_tag + 1) && dev_done(CS_D2H, q.d2h) &&
+             dev_done(CS_H2D, q.h2d));
   });
   for (auto it = keep_b; it != block_q_.end(); ++it) free_blocks_.push_back(it->id);
   block_q_.erase(keep_b, block_q_.end());
   auto keep_s = std::stable_partition(slot_q_.begin(), slot_q_.end(), [&](const Quarantined& q) {
-    return !(job_prefix_done(CS_D2H, q.d2h_tag) && job_prefix_done(CS_H2D, q.h2d_tag));
+    return !(dev_done(CS_D2H, q.d2h) && dev_done(CS_H2D, q.h2d));
   });
   for (auto it = keep_s; it != slot_q_.end(); ++it) free_slots_.push_back(it->id);
   slot_q_.erase(keep_s, slot_q_.end());
+}
+
+std::pair<int32_t, int64_t> BlockPool::job_device(int64_t job_id) const {
+  auto f = job_dev_.find(job_id);
+  if (f == job_dev_.end()) {
+    if (job_id >= 1 && job_id < next_job_) return {CS_D2H, 0};
+    throw LogicError("unknown transfer job");
+  }
+  return f->second;
 }
 
 void BlockPool::on_forward_completed() {
@@ -191,6 +246,7 @@ cs_alloc_result BlockPool::allocate(int64_t id, int64_t n_tokens) {
       p.on_gpu = true;
       p.host_tokens = 0;
       p.recompute_on_evict = false;
+      ++p.gen;  // any D2H of the old contents still in flight is stale now
       p.block = take_block();
       gpu_used_ += p.tokens * bpt;
       r.gpu_tokens += p.tokens;
@@ -469,6 +525,7 @@ std::optional<cs_transfer_job> BlockPool::flush_checkpoints(int64_t now) {
     if (p.slot < 0) p.slot = take_slot();
     bytes += db;
     accepted.push_back(d);
+    accepted.back().gen = p.gen;
   }
   staged_.clear();
   if (accepted.empty()) return std::nullopt;
@@ -507,9 +564,8 @@ std::optional<cs_transfer_job> BlockPool::flush_checkpoints(int64_t now) {
   Job job;
   job.info = info;
   job.deltas = std::move(accepted);
-  job_ordinal_[info.id] = ++issued_[CS_D2H];
-  done_[CS_D2H].push_back(false);
-  if (mover_ != nullptr && !segs.empty()) job.launched = mover_->gather_to_host(info.id, segs);
+  job.dev = launch_gather(segs);
+  job_dev_[info.id] = {CS_D2H, job.dev};
   jobs_.emplace(info.id, std::move(job));
   return info;
 }
@@ -575,9 +631,8 @@ std::optional<cs_transfer_job> BlockPool::start_prefetch(int64_t id, int64_t now
   Job job;
   job.info = info;
   for (size_t i : targets) job.restores.emplace_back(id, i);
-  job_ordinal_[info.id] = ++issued_[CS_H2D];
-  done_[CS_H2D].push_back(false);
-  if (mover_ != nullptr) job.launched = mover_->scatter_from_host(info.id, segs);
+  job.dev = launch_scatter(segs);
+  job_dev_[info.id] = {CS_H2D, job.dev};
   jobs_.emplace(info.id, std::move(job));
   return info;
 }
@@ -596,16 +651,21 @@ int64_t BlockPool::recompute_chunk(int64_t id, int64_t desired, int64_t cap) con
   return tokens;
 }
 
-// KvCacheManager::on_transfer_done (kv_cache.cpp:471-520). Waits for the
-// real transfer first, so bookkeeping never runs ahead of the bytes.
+// KvCacheManager::on_transfer_done (kv_cache.cpp:471-520). Bookkeeping only:
+// it does not wait for the device (SURVEY.md 8b "Completion"; cs_job_poll /
+// cs_job_wait report the real copy). Blocks and slots stay quarantined until
+// the device jobs touching them complete, a restore waits for the gathers
+// writing its slots, and the forward waits for the restores of the blocks it
+// reads (BlockPool::block_h2d), so logical completion may run ahead of the
+// bytes without any reader seeing them early.
 DoneResult BlockPool::on_transfer_done(int64_t job_id) {
   auto jit = jobs_.find(job_id);
   if (jit == jobs_.end()) throw LogicError("unknown transfer job");
   Job& job = jit->second;
-  if (job.launched && mover_ != nullptr) mover_->wait_job(job_id);
   const int64_t bpt = cfg_.kv_bytes_per_token;
   DoneResult out;
 
+  std::vector<Segment> fixup;
   for (const Delta& d : job.deltas) {
     auto rit = reqs_.find(d.req);
     const int64_t db = (d.to - d.from) * bpt;
@@ -621,6 +681,16 @@ DoneResult BlockPool::on_transfer_done(int64_t job_id) {
     }
     p.host_tokens = d.to;
     if (p.inflight_to == d.to) p.inflight_to = 0;
+    if (p.gen != d.gen) {
+      // The page was discarded and re-materialized (recompute) while this
+      // copy was in flight: the reference counts [0, d.to) as checkpointed,
+      // but the copy landed in a slot the page no longer owns. Re-gather the
+      // recomputed positions into the page's current slot (device-only; the
+      // reference byte counters are unchanged). ADVICE r1 (high).
+      if (p.slot < 0) p.slot = take_slot();
+      if (p.block >= 0) fixup.push_back({p.block, p.slot, 0, static_cast<int32_t>(d.to)});
+      ++fixups_;
+    }
     host_lru_.emplace(++host_stamp_, std::make_pair(d.req, d.page));
     if (p.evict_on_ckpt && p.loc() == Loc::kBoth) {
       drop_gpu_page(r, p);
@@ -641,16 +711,8 @@ DoneResult BlockPool::on_transfer_done(int64_t job_id) {
     const int64_t rid = job.restores.front().first;
     if (reqs_.count(rid) && fully_resident(rid)) out.became_resident.push_back(rid);
   }
-
-  const int32_t dir = job.info.direction;
-  const int64_t ord = job_ordinal_.at(job_id);
-  job_ordinal_.erase(job_id);
-  done_[dir][static_cast<size_t>(ord - 1)] = true;
-  while (done_prefix_[dir] < issued_[dir] && done_[dir][static_cast<size_t>(done_prefix_[dir])]) {
-    ++done_prefix_[dir];
-  }
-  if (job.launched && mover_ != nullptr) mover_->release_job(job_id);
   jobs_.erase(jit);
+  if (!fixup.empty()) launch_gather(fixup);
   reclaim();
   return out;
 }

@@ -44,6 +44,7 @@ struct Page {
   int32_t block = -1;        // physical HBM block while resident / restoring
   int32_t slot = -1;         // host pool slot while it holds host data
   int32_t last_block = -1;   // block held before the last drop (D3 stale reads)
+  uint32_t gen = 0;          // bumped when a discarded page is re-materialized
 
   Loc loc() const {
     if (discarded) return Loc::kDiscarded;
@@ -60,14 +61,20 @@ struct Segment {
   int32_t t1;
 };
 
-// Data movement backend (engine.cu). Jobs are FIFO per direction.
+// Data movement backend (engine.cu). Device jobs are FIFO per direction and
+// numbered 1, 2, ... in issue order (an "ordinal"); the pool never blocks on
+// them. It holds a block or host slot back from reuse only until the last
+// device job that touches it has completed (done_prefix), and orders a
+// restore after the gathers still writing its slots (`after`).
 struct Mover {
   virtual ~Mover() = default;
-  // Return false when nothing was launched (dry replay): no wait needed.
-  virtual bool gather_to_host(int64_t job_id, const std::vector<Segment>& segs) = 0;
-  virtual bool scatter_from_host(int64_t job_id, const std::vector<Segment>& segs) = 0;
-  virtual void wait_job(int64_t job_id) = 0;
-  virtual void release_job(int64_t job_id) = 0;
+  // Launch one device job; `after` = ordinal of a job of the OTHER direction
+  // that must complete first (0: none). Returns the job's ordinal, or 0 when
+  // nothing was launched (dry replay).
+  virtual int64_t gather_to_host(const std::vector<Segment>& segs, int64_t after_h2d) = 0;
+  virtual int64_t scatter_from_host(const std::vector<Segment>& segs, int64_t after_d2h) = 0;
+  // Every job of `dir` with ordinal <= the result has completed on the device.
+  virtual int64_t done_prefix(int32_t dir) = 0;
 };
 
 struct PoolConfig {
@@ -109,13 +116,14 @@ struct Delta {
   // been written yet. w1 < 0: identity (no forward noted, bookkeeping only).
   int64_t shift = 0;
   int64_t w1 = -1;
+  uint32_t gen = 0;  // page generation at flush: a re-materialized page's old copy is stale
 };
 
 struct Job {
   cs_transfer_job info{};
   std::vector<Delta> deltas;                          // D2H payload
   std::vector<std::pair<int64_t, size_t>> restores;   // H2D payload
-  bool launched = false;
+  int64_t dev = 0;                                    // device ordinal (0: nothing launched)
 };
 
 struct ReleaseResult {
@@ -164,6 +172,13 @@ class BlockPool {
   int64_t total_h2d() const { return total_h2d_; }
   int64_t recompute_tagged() const { return recompute_tagged_; }
   bool transfers_inflight() const { return !jobs_.empty(); }
+  // Device ordinal of a reference job (dir, ordinal); ordinal 0 when it moved
+  // nothing on the device. Known for every job id issued so far.
+  std::pair<int32_t, int64_t> job_device(int64_t job_id) const;
+  // Device ordinal of the last restore that wrote block b (the forward that
+  // reads b must be ordered after it).
+  int64_t block_h2d(int32_t b) const { return blk_h2d_[static_cast<size_t>(b)]; }
+  int64_t fixup_gathers() const { return fixups_; }
   int64_t request_gpu_pages(int64_t id) const;
   int64_t covered_tokens(int64_t id) const;
   int64_t pending_append_tokens(int64_t id) const;
@@ -198,8 +213,8 @@ class BlockPool {
   struct Quarantined {
     int32_t id;
     uint64_t fwd_tag;  // forwards launched at retire time
-    int64_t d2h_tag;   // D2H jobs issued at retire time
-    int64_t h2d_tag;
+    int64_t d2h;       // last device gather touching it (0: none)
+    int64_t h2d;       // last device restore touching it
   };
 
   Req& req(int64_t id);
@@ -211,7 +226,9 @@ class BlockPool {
   void retire_block(Page& p);
   void retire_slot(Page& p);
   void reclaim();
-  bool job_prefix_done(int32_t dir, int64_t tag) const;
+  bool dev_done(int32_t dir, int64_t ord);
+  int64_t launch_gather(const std::vector<Segment>& segs);
+  int64_t launch_scatter(const std::vector<Segment>& segs);
 
   PoolConfig cfg_;
   Mover* mover_;
@@ -229,12 +246,12 @@ class BlockPool {
   std::vector<int32_t> free_blocks_, free_slots_;  // LIFO stacks
   std::vector<Quarantined> block_q_, slot_q_;
   uint64_t fwd_launched_ = 0, fwd_completed_ = 0;
-  // per-direction job ordinals (1-based issue order) and completion flags
-  int64_t issued_[2] = {0, 0};
-  std::vector<bool> done_[2];
-  int64_t done_prefix_[2] = {0, 0};
-  std::map<int64_t, int64_t> job_ordinal_;  // job id -> ordinal in its lane
-  int64_t moved_d2h_ = 0, moved_h2d_ = 0, nonresident_reads_ = 0;
+  // last device job per block / host slot: gathers read blocks and write
+  // slots, restores read slots and write blocks (ordinals per direction)
+  std::vector<int64_t> blk_d2h_, blk_h2d_, slot_d2h_, slot_h2d_;
+  int64_t dev_done_[2] = {0, 0};                        // cached done_prefix
+  std::map<int64_t, std::pair<int32_t, int64_t>> job_dev_;  // job id -> (dir, ordinal)
+  int64_t moved_d2h_ = 0, moved_h2d_ = 0, nonresident_reads_ = 0, fixups_ = 0;
 };
 
 }  // namespace csb

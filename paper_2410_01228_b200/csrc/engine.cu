@@ -2,11 +2,11 @@
 // layer forward and the checkpoint/restore data movement.
 //
 // Streams: compute (forward), d2h (checkpoint gather), h2d (restore). The
-// forward is enqueued layer by layer; when the iteration carries offline work
-// and the policy is instrumented, a worker thread paces the enqueue
-// `layer_lookahead` layers ahead of the device so the host can shrink the
-// GEMM M dimension once a preemption flag is seen, while the device-side
-// safepoint kernel truncates every other kernel at the layer boundary itself.
+// whole forward is enqueued at once (or replayed as a CUDA graph); a
+// layer-wise preemption is applied on the device: the safepoint kernel
+// between layers truncates the iteration descriptor to the online prefix and
+// every later kernel -- the K8 GEMMs included -- reads the truncated counts,
+// so no host thread paces the launches.
 #include <cublasLt.h>
 #include <cublas_v2.h>
 #include <cuda.h>
@@ -67,6 +67,9 @@ bool wgemm_supported(int M, int N, int K);
 void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, int Mp, int N, int K, int splits,
               int stages, bool f32_out, cudaStream_t s);
 void p2p_allreduce(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s);
+bool gemm_pf_supported(int N, int K);
+void gemm_pf(const CUtensorMap* xmap, const CUtensorMap* wmap, void* y, int M, const int32_t* m_dev, int N, int K,
+             bool f32_out, int sms, cudaStream_t s);
 }  // namespace csk
 
 namespace {
@@ -181,22 +184,31 @@ namespace {
 struct DeviceMover : csb::Mover {
   cs_engine* e;
   struct Rec {
+    int64_t ord;
     std::shared_ptr<EventPair> ev;
-    int dir;
-    int64_t bytes;
-    bool timed = false;
   };
-  std::map<int64_t, Rec> recs;
+  std::deque<Rec> live[2];          // launched, not yet seen complete (issue order)
+  int64_t issued[2] = {0, 0}, done[2] = {0, 0};
+  std::map<int64_t, float> ms_of[2];  // device ms of recently completed jobs (cs_job_poll)
   explicit DeviceMover(cs_engine* eng) : e(eng) {}
-  bool launch(int dir, int64_t job_id, const std::vector<csb::Segment>& segs);
-  bool gather_to_host(int64_t job_id, const std::vector<csb::Segment>& segs) override {
-    return launch(CS_D2H, job_id, segs);
+  int64_t launch(int dir, const std::vector<csb::Segment>& segs, int64_t after_other);
+  int64_t gather_to_host(const std::vector<csb::Segment>& segs, int64_t after_h2d) override {
+    return launch(CS_D2H, segs, after_h2d);
   }
-  bool scatter_from_host(int64_t job_id, const std::vector<csb::Segment>& segs) override {
-    return launch(CS_H2D, job_id, segs);
+  int64_t scatter_from_host(const std::vector<csb::Segment>& segs, int64_t after_d2h) override {
+    return launch(CS_H2D, segs, after_d2h);
   }
-  void wait_job(int64_t job_id) override;
-  void release_job(int64_t job_id) override { recs.erase(job_id); }
+  int64_t done_prefix(int32_t dir) override {
+    poll(dir);
+    return done[dir];
+  }
+  void poll(int dir);
+  // end event of job `ord` of `dir`, or null once it completed
+  cudaEvent_t pending_event(int dir, int64_t ord) {
+    for (const Rec& r : live[dir])
+      if (r.ord == ord) return r.ev->end;
+    return nullptr;
+  }
 };
 
 }  // namespace
@@ -244,7 +256,6 @@ struct cs_engine {
 
   cudaStream_t s_compute = nullptr, s_d2h = nullptr, s_h2d = nullptr;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_fwd_done = nullptr;
-  std::vector<cudaEvent_t> ev_layer;
   bool any_forward = false;
   cublasHandle_t blas = nullptr;
   void* blas_ws = nullptr;
@@ -282,7 +293,7 @@ struct cs_engine {
     bool active = false;
     uint64_t epoch = 0;
     int n_tok = 0, n_tok_on = 0, n_ent = 0, n_ent_on = 0, n_dec = 0, n_pt = 0;
-    bool has_offline = false, paced = false;
+    bool has_offline = false;
     int splits = 1, pps = 1;
     int k2_splits = 1, k2_tps = 1 << 30;
     bool graph = false;  // decode-only plan replayed from a captured CUDA graph
@@ -293,19 +304,12 @@ struct cs_engine {
     const int32_t* d_tok_ids = nullptr;
     const int32_t* d_tok_slot = nullptr;
     const int32_t* d_ent_last = nullptr;
-    int gemm_trunc_layer = -1;
+    bool device_m = false;  // every layer GEMM is K8 (reads the device row count)
+    int64_t wait_h2d = 0;  // last restore writing a block this plan reads
     uint64_t signal_ns = 0;
     int64_t meta_bytes = 0;
   } it;
 
-  // pacing worker
-  std::thread worker;
-  std::mutex mu;
-  std::condition_variable cv;
-  bool job_ready = false, job_done = true, quit = false;
-  std::string worker_err;
-
-  int64_t layer_gemm_rows(int layer);
   void enqueue_layers();
   int enqueue_body(int Tg, int Eg, bool graph);
   // CUDA graphs of decode-only forwards, keyed by (bucket, safepoints, gen);
@@ -322,7 +326,13 @@ struct cs_engine {
     graphs.clear();
     ++graph_gen;
   }
-  int gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
+  int gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32,
+           const int32_t* m_dev = nullptr);
+  // K8 (csrc/gemm_pf.cu) for this layer GEMM? Prefill-sized M, or any
+  // non-graph M > 256 when a safepoint may truncate the batch on the device
+  bool use_pf(int M, int N, int K) const;
+  int pf_min_rows = 2048;
+  bool pf_enabled = true;
   void allreduce(__nv_bfloat16* buf, int64_t count);
   // ---- peer-memory all-reduce: exchange region =
   // [2 partial buffers of (max_tok*hidden + 64) bf16][flag u64][step u64][arrive i32]
@@ -348,37 +358,43 @@ struct cs_engine {
 
 namespace {
 
-bool DeviceMover::launch(int dir, int64_t job_id, const std::vector<csb::Segment>& segs) {
-  if (e->dry) return false;
-  Rec r;
-  r.ev = std::make_shared<EventPair>();
-  r.dir = dir;
-  r.bytes = 0;
+int64_t DeviceMover::launch(int dir, const std::vector<csb::Segment>& segs, int64_t after_other) {
+  if (e->dry || segs.empty()) return 0;
+  auto ev = std::make_shared<EventPair>();
   const size_t n = segs.size() * sizeof(csb::Segment);
   DescRing& ring = e->ring[dir];
-  const size_t off = ring.alloc(n, r.ev);
+  const size_t off = ring.alloc(n, ev);
   std::memcpy(ring.host + off, segs.data(), n);
   cudaStream_t st = dir == CS_D2H ? e->s_d2h : e->s_h2d;
+  // a gather reads KV the last forward wrote; either direction may have to
+  // follow a job of the other one that touches the same block / host slot
   if (dir == CS_D2H && e->any_forward) CK(cudaStreamWaitEvent(st, e->ev_fwd_done, 0));
-  CK(cudaEventRecord(r.ev->start, st));
+  if (after_other > 0) {
+    if (cudaEvent_t w = pending_event(1 - dir, after_other)) CK(cudaStreamWaitEvent(st, w, 0));
+  }
+  CK(cudaEventRecord(ev->start, st));
   csk::kv_move(dir == CS_D2H, e->kv, e->host_kv_dev, ring.dev + off, static_cast<int>(segs.size()),
                e->L * 2 * e->hkv, e->D, e->sms, st);
   e->launches += 1;
   CK(cudaGetLastError());
-  CK(cudaEventRecord(r.ev->end, st));
-  recs.emplace(job_id, std::move(r));
-  return true;
+  CK(cudaEventRecord(ev->end, st));
+  live[dir].push_back({++issued[dir], std::move(ev)});
+  return issued[dir];
 }
 
-void DeviceMover::wait_job(int64_t job_id) {
-  auto it = recs.find(job_id);
-  if (it == recs.end()) return;
-  CK(cudaEventSynchronize(it->second.ev->end));
-  if (!it->second.timed) {
+void DeviceMover::poll(int dir) {
+  while (!live[dir].empty()) {
+    const Rec& r = live[dir].front();
+    const cudaError_t q = cudaEventQuery(r.ev->end);
+    if (q == cudaErrorNotReady) break;
+    CK(q);
     float ms = 0;
-    CK(cudaEventElapsedTime(&ms, it->second.ev->start, it->second.ev->end));
-    e->moved_ms[it->second.dir] += ms;
-    it->second.timed = true;
+    CK(cudaEventElapsedTime(&ms, r.ev->start, r.ev->end));
+    e->moved_ms[dir] += ms;
+    ms_of[dir][r.ord] = ms;
+    if (ms_of[dir].size() > 4096) ms_of[dir].erase(ms_of[dir].begin());
+    done[dir] = r.ord;
+    live[dir].pop_front();
   }
 }
 
@@ -618,9 +634,28 @@ bool cs_engine::wgemm_launch(const __nv_bfloat16* A, const __nv_bfloat16* W, voi
   return true;
 }
 
-// Returns the number of hand-written kernels it launched (K7: 1, cuBLAS: 0).
-int cs_engine::gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32) {
+bool cs_engine::use_pf(int M, int N, int K) const {
+  if (!pf_enabled || !csk::gemm_pf_supported(N, K)) return false;
+  if (M >= pf_min_rows) return true;
+  // the device-side row count is what makes a layer-wise drop shrink the
+  // GEMMs of the remaining layers: worth K8's small-M cost when one may come
+  return M > 256 && cfg.instrumented != 0 && it.has_offline && !it.graph;
+}
+
+// Returns the number of hand-written kernels it launched (K7/K8: 1, cuBLAS: 0).
+// m_dev: device row count (IterDesc.n_tok_cur) honoured by K8.
+int cs_engine::gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32,
+                    const int32_t* m_dev) {
   if (M <= 0) return 0;
+  if (use_pf(M, N, K)) {
+    const int rows = A == xl ? static_cast<int>(max_ent) : static_cast<int>(max_tok);
+    const CUtensorMap* xm = tmap(A, rows, K, 128);
+    const CUtensorMap* wm = tmap(W, N, K, 128);
+    if (xm && wm) {
+      csk::gemm_pf(xm, wm, C, M, m_dev, N, K, out_f32, sms, s_compute);
+      return 1;
+    }
+  }
   if (wgemm(A, W, C, M, N, K, out_f32)) return 1;
   if (lt_gemm(A, W, C, M, N, K, out_f32)) return 0;
   const float alpha = 1.f, beta = 0.f;
@@ -656,20 +691,14 @@ void cs_engine::reduce_into(__nv_bfloat16* buf, int64_t count) {
   part_slot ^= 1;
 }
 
-// GEMM rows for a layer: all token rows until the host has observed a drop.
-// Tokens are ordered online-first, so truncation is a prefix of the rows.
-int64_t cs_engine::layer_gemm_rows(int layer) {
-  if (it.gemm_trunc_layer >= 0 && layer >= it.gemm_trunc_layer) return it.n_tok_on;
-  return it.n_tok;
-}
-
 // Enqueues the layer stack and the head for Tg token rows / Eg entries (the
 // plan's counts, or the graph bucket's); returns the kernels it launched.
 int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   int n_launch = 0;
   const auto* desc = reinterpret_cast<const csk::IterDesc*>(d_meta);
   auto* desc_mut = reinterpret_cast<csk::IterDesc*>(d_meta);
-  const int lookahead = cfg.layer_lookahead > 0 ? cfg.layer_lookahead : 2;
+  // K8 GEMMs read the live row count: a safepoint drop shrinks them too
+  const int32_t* m_dev = &desc->n_tok_cur;
   const bool instrumented = cfg.instrumented != 0 && it.has_offline;
   const int qkv_cols = (hq + 2 * hkv) * D;
   const int T = Tg;
@@ -677,19 +706,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   auto is_sp = [&](int l) { return instrumented && l > 0 && l < L && l % cfg.safepoint_interval_layers == 0; };
 
   for (int l = 0; l < L; ++l) {
-    if (it.paced && l > lookahead) CK(cudaEventSynchronize(ev_layer[l - lookahead - 1]));
-    if (is_sp(l) && !graph) {
-      // Host view of the flag: once seen, later layers' GEMMs shrink to the
-      // online rows (the device truncates everything else at this layer).
-      if (tp == 1) {
-        if (it.gemm_trunc_layer < 0 && mailbox->flag_epoch == it.epoch) it.gemm_trunc_layer = l;
-      } else if (it.gemm_trunc_layer < 0 && mailbox->seen_epoch == it.epoch && mailbox->seen_layer >= 0 &&
-                 mailbox->seen_layer <= l - lookahead - 1) {
-        // TP: follow the device-agreed drop layer, deterministic on all ranks.
-        it.gemm_trunc_layer = l;
-      }
-    }
-    const int64_t M = graph ? Tg : layer_gemm_rows(l);
+    const int64_t M = Tg;
     if (l == 0) {
       csk::embed(x, w.emb, it.d_tok_ids, hidden, desc, T, s_compute);
     }
@@ -701,7 +718,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
       }
     }
     csk::add_rmsnorm(x, l == 0 ? nullptr : tmp, w.attn_norm[l], xn, hidden, cfg.rms_eps, desc, nullptr, T, s_compute);
-    n_launch += gemm(xn, w.wqkv[l], qkv, static_cast<int>(M), qkv_cols, hidden, false);
+    n_launch += gemm(xn, w.wqkv[l], qkv, static_cast<int>(M), qkv_cols, hidden, false, m_dev);
     csk::rope_append(qkv, it.ap.tok_pos, it.d_tok_slot, kv, hq, hkv, D, L, l,
                      cfg.rope_theta, desc, T, s_compute);
     csk::AttnParams ap = it.ap;
@@ -710,16 +727,16 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
       throw ConfigError("unsupported attention shape");
     {
       __nv_bfloat16* part = partial_out(tmp);
-      n_launch += gemm(attn, w.wo[l], part, static_cast<int>(M), hidden, hq * D, false);
+      n_launch += gemm(attn, w.wo[l], part, static_cast<int>(M), hidden, hq * D, false, m_dev);
       if (part != tmp) ++n_launch;
       reduce_into(tmp, M * hidden);
     }
     csk::add_rmsnorm(x, tmp, w.mlp_norm[l], xn, hidden, cfg.rms_eps, desc, nullptr, T, s_compute);
-    n_launch += gemm(xn, w.wgu[l], gu, static_cast<int>(M), 2 * ffn, hidden, false);
+    n_launch += gemm(xn, w.wgu[l], gu, static_cast<int>(M), 2 * ffn, hidden, false, m_dev);
     csk::silu_mul(gu, act, ffn, desc, T, s_compute);
     {
       __nv_bfloat16* part = partial_out(tmp);
-      n_launch += gemm(act, w.wd[l], part, static_cast<int>(M), hidden, ffn, false);
+      n_launch += gemm(act, w.wd[l], part, static_cast<int>(M), hidden, ffn, false, m_dev);
       if (tp > 1) {
         if (part != tmp) ++n_launch;
         if (is_sp(l + 1)) {
@@ -734,7 +751,6 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
     }
     n_launch += (l == 0 ? 1 : 0) + (is_sp(l) ? 1 : 0) + 4 + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
                 (it.n_dec > 0 ? 1 : 0) + (it.n_pt > 0 ? (it.k2_splits > 1 ? 2 : 1) : 0);
-    if (it.paced) CK(cudaEventRecord(ev_layer[l], s_compute));
     if ((cfg.flags & CS_FLAG_SYNC_DEBUG) && !graph) {
       CK(cudaStreamSynchronize(s_compute));
       CK(cudaGetLastError());
@@ -753,7 +769,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   return n_launch;
 }
 
-// Enqueues every layer of the current iteration (caller or worker thread).
+// Enqueues every layer of the current iteration.
 // Decode-only plans run a CUDA graph captured once per bucket: all per-plan
 // data (counts, split sizes, block tables) is read from the device metadata,
 // so one graph serves every plan of its bucket and the ~350 launches of a
@@ -849,7 +865,10 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
       ent_kvlen[i] = kv_len;
       ent_bt[i] = static_cast<int32_t>(bt.size());
       const int n_pages = (kv_len + 15) / 16;
-      for (int pg = 0; pg < n_pages; ++pg) bt.push_back(pool.block_for_read(be.request_id, static_cast<size_t>(pg)));
+      for (int pg = 0; pg < n_pages; ++pg) {
+        bt.push_back(pool.block_for_read(be.request_id, static_cast<size_t>(pg)));
+        it.wait_h2d = std::max(it.wait_h2d, pool.block_h2d(bt.back()));
+      }
       for (int32_t p : pos) {
         tok_ids.push_back(csk::token_id(e->cfg.token_seed, be.request_id, p, e->vocab));
         tok_pos.push_back(p);
@@ -888,10 +907,8 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     it.n_pt = static_cast<int>(tiles.size());
     it.has_offline = seen_offline;
     pool.on_forward_launched();
-    if (e->host_only || e->no_model || e->dry) {
-      it.active = true;
-      return false;
-    }
+    it.active = true;  // from here on an error must end the iteration (cs_forward_launch)
+    if (e->host_only || e->no_model || e->dry) return false;
 
     // ---- graph mode: decode-only plans of <= 256 rows replay a captured
     // CUDA graph of their bucket (sizes padded; kernels skip rows >= *_cur)
@@ -1154,8 +1171,6 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
       CK(cudaEventCreate(&e->ev_start));
       CK(cudaEventCreate(&e->ev_end));
       CK(cudaEventCreateWithFlags(&e->ev_fwd_done, cudaEventDisableTiming));
-      e->ev_layer.resize(static_cast<size_t>(e->L));
-      for (auto& ev : e->ev_layer) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
 
       const size_t blk_bytes = static_cast<size_t>(e->block_elems) * 2;
       CK(cudaMalloc(&e->kv, static_cast<size_t>(pc.n_blocks) * blk_bytes));
@@ -1316,12 +1331,6 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
 int cs_destroy(cs_engine* e) {
   if (!e) return CS_OK;
   return guard([&] {
-    {
-      std::lock_guard<std::mutex> lk(e->mu);
-      e->quit = true;
-    }
-    e->cv.notify_all();
-    if (e->worker.joinable()) e->worker.join();
     if (!e->host_only) {
       cudaDeviceSynchronize();
       e->drop_graphs();
@@ -1356,7 +1365,6 @@ int cs_destroy(cs_engine* e) {
       cudaEventDestroy(e->ev_start);
       cudaEventDestroy(e->ev_end);
       cudaEventDestroy(e->ev_fwd_done);
-      for (auto& ev : e->ev_layer) cudaEventDestroy(ev);
       cudaStreamDestroy(e->s_compute);
       cudaStreamDestroy(e->s_d2h);
       cudaStreamDestroy(e->s_h2d);
@@ -1514,6 +1522,35 @@ int cs_kv_on_transfer_done(cs_engine* e, int64_t job_id, int64_t now, cs_transfe
     for (size_t i = 0; i < r.became_resident.size() && i < 4; ++i) out->became_resident[i] = r.became_resident[i];
   });
 }
+// Real completion of a reference transfer job (SURVEY.md 8b "Completion"):
+// done = its device copy finished; *ms = the copy's device time (-1 while
+// running, 0 when it moved nothing on the device).
+static void job_state(cs_engine* e, int64_t job_id, bool wait, int32_t* done, double* ms) {
+  const auto [dir, ord] = e->pool->job_device(job_id);
+  *done = 1;
+  if (ms) *ms = 0;
+  if (ord == 0 || !e->mover) return;
+  if (wait) {
+    if (cudaEvent_t ev = e->mover->pending_event(dir, ord)) CK(cudaEventSynchronize(ev));
+  }
+  e->mover->poll(dir);
+  if (e->mover->done[dir] < ord) {
+    *done = 0;
+    if (ms) *ms = -1;
+    return;
+  }
+  auto f = e->mover->ms_of[dir].find(ord);
+  if (ms) *ms = f == e->mover->ms_of[dir].end() ? -1 : f->second;
+}
+int cs_job_poll(cs_engine* e, int64_t job_id, int32_t* done, double* ms) {
+  return guard([&] { job_state(e, job_id, false, done, ms); });
+}
+int cs_job_wait(cs_engine* e, int64_t job_id, double* ms) {
+  return guard([&] {
+    int32_t d = 0;
+    job_state(e, job_id, true, &d, ms);
+  });
+}
 int cs_kv_on_request_paused(cs_engine* e, int64_t id, uint64_t seq) {
   return guard([&] { e->pool->on_request_paused(id, seq); });
 }
@@ -1524,6 +1561,10 @@ int cs_kv_note_written(cs_engine* e, int64_t id, int64_t w0, int64_t w1) {
 }
 int cs_kv_stats_get(cs_engine* e, cs_kv_stats* o) {
   return guard([&] {
+    if (e->mover) {
+      e->mover->poll(CS_D2H);
+      e->mover->poll(CS_H2D);
+    }
     const csb::BlockPool& p = *e->pool;
     o->gpu_used_bytes = p.gpu_used();
     o->gpu_free_bytes = p.gpu_free();
@@ -1580,56 +1621,27 @@ int cs_kv_block_table(cs_engine* e, int64_t id, int32_t* blocks, int32_t* slots,
 
 // ---------------------------------------------------------------- forward --
 int cs_forward_launch(cs_engine* e, const cs_batch_entry* entries, int32_t n, uint64_t epoch) {
-  return guard([&] {
+  const int rc = guard([&] {
     if (!prepare_iteration(e, entries, n, epoch)) return;
     auto& it = e->it;
+    // restores the reference already counts complete may still be copying:
+    // the forward (not the host) waits for the ones writing blocks it reads
+    if (it.wait_h2d > 0 && e->mover && e->mover->done_prefix(CS_H2D) < it.wait_h2d) {
+      if (cudaEvent_t w = e->mover->pending_event(CS_H2D, it.wait_h2d)) CK(cudaStreamWaitEvent(e->s_compute, w, 0));
+    }
     CK(cudaEventRecord(e->ev_start, e->s_compute));
     CK(cudaMemcpyAsync(e->d_meta, e->h_meta, static_cast<size_t>(it.meta_bytes), cudaMemcpyHostToDevice,
                        e->s_compute));
     e->any_forward = true;
     it.active = true;
-    // CS_NO_PACING=1 (profilers that serialise launches across threads):
-    // enqueue every layer from the caller; the device safepoint still drops
-    // offline work, only the host-side GEMM shrink is lost.
-    static const bool no_pacing = [] {
-      const char* v = std::getenv("CS_NO_PACING");
-      return v && v[0] == '1';
-    }();
-    it.paced = e->cfg.instrumented != 0 && it.has_offline && e->L > 1 && !no_pacing && !it.graph;
-    if (!it.paced) {
-      e->enqueue_layers();
-      return;
-    }
-    // paced: hand the layer loop to the worker thread
-    if (!e->worker.joinable()) {
-      e->worker = std::thread([e] {
-        std::unique_lock<std::mutex> lk(e->mu);
-        for (;;) {
-          e->cv.wait(lk, [e] { return e->job_ready || e->quit; });
-          if (e->quit) return;
-          e->job_ready = false;
-          lk.unlock();
-          std::string err;
-          try {
-            CK(cudaSetDevice(e->cfg.device));
-            e->enqueue_layers();
-          } catch (const std::exception& ex) {
-            err = ex.what();
-          }
-          lk.lock();
-          e->worker_err = err;
-          e->job_done = true;
-          e->cv.notify_all();
-        }
-      });
-    }
-    {
-      std::lock_guard<std::mutex> lk(e->mu);
-      e->job_done = false;
-      e->job_ready = true;
-    }
-    e->cv.notify_all();
+    it.device_m = e->use_pf(it.n_tok, (e->hq + 2 * e->hkv) * e->D, e->hidden) && !it.graph;
+    e->enqueue_layers();
   });
+  if (rc != CS_OK && e->it.active) {  // balance the pool's forward counters
+    e->it.active = false;
+    e->pool->on_forward_completed();
+  }
+  return rc;
 }
 
 // Times the paged-attention kernels alone (layer 0) for one plan: reps
@@ -1748,13 +1760,6 @@ int cs_iter_poll(cs_engine* e, int32_t* done) {
       *done = 1;
       return;
     }
-    {
-      std::lock_guard<std::mutex> lk(e->mu);
-      if (!e->job_done) {
-        *done = 0;
-        return;
-      }
-    }
     const cudaError_t q = cudaEventQuery(e->ev_end);
     if (q == cudaErrorNotReady) {
       *done = 0;
@@ -1769,21 +1774,22 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
   return guard([&] {
     auto& it = e->it;
     if (!it.active) throw std::logic_error("no iteration in flight");
+    // any exit (CUDA error included) ends the iteration and balances the
+    // pool's launched/completed forward counters
+    struct End {
+      cs_engine* e;
+      bool done = false;
+      ~End() {
+        if (done) return;
+        e->it.active = false;
+        e->pool->on_forward_completed();
+      }
+    } end{e};
     cs_iter_info inf{};
     inf.preempted_at_layer = -1;
     inf.gemm_trunc_layer = -1;
     int n_alive = it.n_ent;
     if (!(e->host_only || e->no_model || e->dry)) {
-      {
-        std::unique_lock<std::mutex> lk(e->mu);
-        e->cv.wait(lk, [e] { return e->job_done; });
-        if (!e->worker_err.empty()) {
-          const std::string err = e->worker_err;
-          e->worker_err.clear();
-          it.active = false;
-          throw CudaError(err);
-        }
-      }
       CK(cudaEventSynchronize(e->ev_end));
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, e->ev_start, e->ev_end));
@@ -1802,7 +1808,9 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
       inf.n_outputs = n_alive;
       inf.h2d_bytes = it.meta_bytes;
       inf.d2h_bytes = static_cast<int64_t>(sizeof(csk::IterDesc) + sizeof(uint64_t) * (it.graph ? it.bucket : it.n_ent));
-      inf.gemm_trunc_layer = it.gemm_trunc_layer;
+      // K8 layer GEMMs follow the device drop: the first layer after the
+      // safepoint already runs every kernel on the truncated batch
+      inf.gemm_trunc_layer = it.device_m ? inf.preempted_at_layer : -1;
       if (out_tokens)
         for (int i = 0; i < n_alive && i < cap; ++i)
           out_tokens[i] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(keys[i] & 0xFFFFFFFFull));
@@ -1818,6 +1826,7 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
       const auto& wr = it.writes[static_cast<size_t>(i)];
       if (wr[1] >= 0 && e->pool->find(wr[0])) e->pool->note_written(wr[0], wr[1], wr[2]);
     }
+    end.done = true;
     e->pool->on_forward_completed();
     it.active = false;
     if (info) *info = inf;

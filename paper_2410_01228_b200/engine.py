@@ -271,6 +271,18 @@ class KvPool:
         return TransferDoneEffects([d.became_resident[i] for i in range(min(d.n_became_resident, 4))],
                                    d.freed_pages)
 
+    def job_poll(self, job_id: int):
+        """(done, device ms) of a transfer job's real copy (cs_job_poll)."""
+        d, ms = C.c_int32(), C.c_double()
+        _check(_lib.cs_job_poll(self._h, job_id, C.byref(d), C.byref(ms)))
+        return bool(d.value), ms.value
+
+    def job_wait(self, job_id: int) -> float:
+        """Blocks until the job's device copy finished; returns its device ms."""
+        ms = C.c_double()
+        _check(_lib.cs_job_wait(self._h, job_id, C.byref(ms)))
+        return ms.value
+
     def on_request_paused(self, rid: int, pause_seq: int) -> None:
         _check(_lib.cs_kv_on_request_paused(self._h, rid, pause_seq))
 

@@ -7,7 +7,17 @@
 // counts and both audits. Also checks the physical invariants (every resident
 // page owns a distinct block; no block or slot leaks) via the pool's audit.
 //
+// Physical content model: a SimMover carries a tag per (block | host slot,
+// token) -- tag(req, pos) is written when an allocation covers a position
+// (the forward that computes it), gathers copy block -> slot, restores slot ->
+// block, synchronously. After every call every GPU-resident page's block must
+// hold tag(req, pos) for all its tokens and every page's host slot for its
+// first host_tokens tokens: a checkpoint or restore that moves the wrong
+// bytes is caught even when the page tables agree with the reference.
+//
 // usage: shadow_fuzz <seed> <ops> [incremental=1] [host_pages=256] [gpu_pages=64]
+//        seed 0: the directed ADVICE r1 sequence (late partial checkpoint of a
+//        page that was discarded and recomputed while its copy was in flight)
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -20,6 +30,27 @@
 #include "block_pool.h"
 
 using namespace coserve;
+
+struct SimMover : csb::Mover {
+  std::vector<std::vector<int64_t>> blk, slot;  // [id][16] content tags (-1 = garbage)
+  int64_t issued[2] = {0, 0};
+  SimMover(int64_t n_blocks, int64_t n_slots)
+      : blk(static_cast<size_t>(n_blocks), std::vector<int64_t>(16, -1)),
+        slot(static_cast<size_t>(n_slots), std::vector<int64_t>(16, -1)) {}
+  int64_t gather_to_host(const std::vector<csb::Segment>& segs, int64_t) override {
+    for (const auto& g : segs)
+      for (int t = g.t0; t < g.t1; ++t) slot[g.slot][t] = blk[g.block][t];
+    return ++issued[0];
+  }
+  int64_t scatter_from_host(const std::vector<csb::Segment>& segs, int64_t) override {
+    for (const auto& g : segs)
+      for (int t = g.t0; t < g.t1; ++t) blk[g.block][t] = slot[g.slot][t];
+    return ++issued[1];
+  }
+  int64_t done_prefix(int32_t dir) override { return issued[dir]; }
+};
+
+static int64_t tag(int64_t req, int64_t pos) { return req * 1000003 + pos; }
 
 static int g_fail = 0;
 #define EXPECT(cond, ...)                                   \
@@ -90,7 +121,8 @@ int main(int argc, char** argv) {
   pc.n_blocks = gpu_pages * 8 + ops / 4 + 64;
   pc.n_slots = host_pages * 4 + ops / 4 + 64;
   pc.moved_bytes_per_token = c.kv_bytes_per_token;
-  csb::BlockPool pool(pc, nullptr);
+  SimMover sim(pc.n_blocks, pc.n_slots);
+  csb::BlockPool pool(pc, &sim);
 
   std::mt19937_64 rng(seed);
   auto rnd = [&](int64_t lo, int64_t hi) {  // inclusive
@@ -111,7 +143,36 @@ int main(int argc, char** argv) {
     return ids[static_cast<size_t>(rnd(0, static_cast<int64_t>(ids.size()) - 1))];
   };
 
+  // the forward of an allocation writes the KV of every position it covers
+  auto write_growth = [&](int64_t id) {
+    const csb::Req* r = pool.find(id);
+    for (const csb::Growth& g : r->growth) {
+      const csb::Page& p = r->pages[g.page];
+      if (p.block < 0) continue;
+      for (int64_t t = g.was_discarded ? 0 : g.prev_tokens; t < p.tokens; ++t)
+        sim.blk[p.block][t] = tag(id, static_cast<int64_t>(g.page) * 16 + t);
+    }
+  };
+  auto check_content = [&](const char* op) {
+    for (auto& [id, on] : live) {
+      const csb::Req* r = pool.find(id);
+      for (size_t i = 0; i < r->pages.size(); ++i) {
+        const csb::Page& p = r->pages[i];
+        if (p.on_gpu && !p.discarded)
+          for (int64_t t = 0; t < p.tokens; ++t)
+            EXPECT(sim.blk[p.block][t] == tag(id, static_cast<int64_t>(i) * 16 + t),
+                   "%s: block %d of req %lld page %zu holds wrong KV at %lld", op, p.block, (long long)id, i,
+                   (long long)t);
+        if (p.host_tokens > 0 && p.slot >= 0)
+          for (int64_t t = 0; t < p.host_tokens; ++t)
+            EXPECT(sim.slot[p.slot][t] == tag(id, static_cast<int64_t>(i) * 16 + t),
+                   "%s: host slot %d of req %lld page %zu holds wrong KV at %lld", op, p.slot, (long long)id, i,
+                   (long long)t);
+      }
+    }
+  };
   auto compare_state = [&](const char* op) {
+    check_content(op);
     EXPECT(ref.gpu_used_bytes() == pool.gpu_used(), "%s gpu_used %lld vs %lld", op,
            (long long)ref.gpu_used_bytes(), (long long)pool.gpu_used());
     EXPECT(ref.host_used_bytes() == pool.host_used(), "%s host_used %lld vs %lld", op,
@@ -147,6 +208,72 @@ int main(int argc, char** argv) {
     }
   };
 
+  if (seed == 0) {
+    // tail checkpoint in flight (inflight_to 4), the tail
+    // grows, evict pass 2 discards the page and frees its slot, recompute
+    // re-materializes it, then the old copy completes.
+    auto both = [&](const char* op, auto&& fr, auto&& fp) {
+      Outcome oa = run(fr), ob = run(fp);
+      EXPECT(oa.kind == ob.kind && oa.msg == ob.msg, "%s outcome '%s' vs '%s'", op, oa.msg.c_str(), ob.msg.c_str());
+      compare_state(op);
+    };
+    ref.register_request(0, false);
+    pool.register_request(0, false);
+    live[0] = false;
+    both("allocate 20", [&] { ref.allocate(0, 20, 0); }, [&] { pool.allocate(0, 20); write_growth(0); });
+    both("commit", [&] { ref.commit_allocations(0); }, [&] { pool.commit(0); });
+    both("stage", [&] { ref.stage_checkpoint(0, 0, 20); }, [&] { pool.stage_checkpoint(0, 0, 20); });
+    int64_t jid = -1;
+    both("flush", [&] { jid = ref.flush_checkpoints(0)->id; }, [&] { pool.flush_checkpoints(0); });
+    both("allocate 2", [&] { ref.allocate(0, 2, 0); }, [&] { pool.allocate(0, 2); write_growth(0); });
+    both("commit", [&] { ref.commit_allocations(0); }, [&] { pool.commit(0); });
+    both("pause", [&] { ref.on_request_paused(0, 1); }, [&] { pool.on_request_paused(0, 1); });
+    both("evict", [&] { ref.evict_request_gpu(0, 0, -1); }, [&] { pool.evict_request_gpu(0, -1); });
+    both("active", [&] { ref.on_request_active(0); }, [&] { pool.on_request_active(0); });
+    both("recompute allocate", [&] { ref.allocate(0, 6, 0); }, [&] { pool.allocate(0, 6); write_growth(0); });
+    both("commit", [&] { ref.commit_allocations(0); }, [&] { pool.commit(0); });
+    both("transfer done", [&] { ref.on_transfer_done(jid, 100000); }, [&] { pool.on_transfer_done(jid); });
+    // the page now counts [0,4) as checkpointed: finish it and bring it back from host
+    both("stage rest", [&] { ref.stage_checkpoint(0, 16, 22); }, [&] { pool.stage_checkpoint(0, 16, 22); });
+    int64_t j2 = -1;
+    both("flush 2", [&] { j2 = ref.flush_checkpoints(1)->id; }, [&] { pool.flush_checkpoints(1); });
+    both("transfer done 2", [&] { ref.on_transfer_done(j2, 200000); }, [&] { pool.on_transfer_done(j2); });
+    both("pause", [&] { ref.on_request_paused(0, 2); }, [&] { pool.on_request_paused(0, 2); });
+    both("evict all", [&] { ref.evict_request_gpu(0, 0, -1); }, [&] { pool.evict_request_gpu(0, -1); });
+    int64_t j3 = -1;
+    both("prefetch", [&] { j3 = ref.start_prefetch(0, 300000)->id; }, [&] { pool.start_prefetch(0, 300000); });
+    both("transfer done 3", [&] { ref.on_transfer_done(j3, 400000); }, [&] { pool.on_transfer_done(j3); });
+    // blocks freed by one request must not wait behind an
+    // unrelated checkpoint that is still copying on the device. 64-page pool
+    // with 2 spare blocks; request 1 has a checkpoint in flight (never
+    // completes here); request 2 releases 40 pages; 39 fresh pages for
+    // request 3 must come from request 2's blocks.
+    struct Pending : SimMover {
+      using SimMover::SimMover;
+      int64_t done_prefix(int32_t) override { return 0; }
+    } pend(66, 64);
+    csb::PoolConfig pc2 = pc;
+    pc2.gpu_capacity = c.kv_bytes_per_token * 16 * 64;
+    pc2.n_blocks = 66;
+    pc2.n_slots = 64;
+    pc2.fwd_quarantine = false;
+    csb::BlockPool p2(pc2, &pend);
+    p2.register_request(1, false);
+    p2.register_request(2, false);
+    p2.register_request(3, false);
+    p2.allocate(1, 16);
+    p2.commit(1);
+    p2.stage_checkpoint(1, 0, 16);
+    p2.flush_checkpoints(0);
+    p2.allocate(2, 40 * 16);
+    p2.commit(2);
+    p2.release_request(2);
+    Outcome o = run([&] { p2.allocate(3, 39 * 16); });
+    EXPECT(o.kind.empty(), "allocate behind an unrelated in-flight checkpoint: %s", o.msg.c_str());
+    std::printf("shadow_fuzz directed failures=%d fixups=%lld\n", g_fail, (long long)pool.fixup_gathers());
+    return g_fail == 0 && pool.fixup_gathers() == 1 ? 0 : 1;
+  }
+
   for (int step = 0; step < ops; ++step) {
     now += rnd(0, 3000);
     const int64_t r = rnd(0, 99);
@@ -170,6 +297,7 @@ int main(int argc, char** argv) {
       if (oa.kind.empty() && ob.kind.empty()) {
         EXPECT(a.ok == (b.ok != 0) && a.shortfall_pages == b.shortfall_pages, "allocate result");
         if (a.ok) uncommitted.insert(id);
+        if (b.ok) write_growth(id);
       }
     } else if (r < 42) {
       op = "commit";

@@ -35,3 +35,25 @@ def test_block_pool_shadows_reference(seed, incremental, host_pages, gpu_pages):
     assert m and int(m.group(1)) == 0, r.stdout + r.stderr[-3000:]
     # the sequence must actually exercise the checkpoint/restore paths
     assert "flush=" in r.stdout and "prefetch=" in r.stdout
+
+
+def test_directed_advice_sequences():
+    """(high) a late partial checkpoint landing on a page that was
+    discarded and recomputed while the copy was in flight must leave the
+    page's host slot holding [0, host_tokens) -- the pool re-gathers it; and
+    (medium) blocks released by one request are reusable while an unrelated
+    checkpoint is still copying. Checked through the content model."""
+    _build()
+    r = subprocess.run([BIN, "0", "1"], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stdout + r.stderr[-3000:]
+    assert "failures=0 fixups=1" in r.stdout
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_block_pool_content_long(seed):
+    """20k random calls on a small host pool (host LRU + recompute fallback)
+    with the physical content model checked after every call."""
+    _build()
+    r = subprocess.run([BIN, str(seed), "20000", "1", "16", "24"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr[-3000:]
+    assert "failures=0" in r.stdout
