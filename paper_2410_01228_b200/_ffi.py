@@ -93,10 +93,18 @@ class cs_batch_entry(C.Structure):
                 ("kind", C.c_int32), ("online", C.c_int32)]
 
 
+class cs_ktime(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("ms", C.c_double), ("units", C.c_double)]
+
+
+CS_KT_K8, CS_KT_K2, CS_KT_K1 = 0, 1, 2
+
+
 class cs_iter_info(C.Structure):
     _fields_ = [("n_outputs", C.c_int32), ("preempted_at_layer", C.c_int32), ("n_entries_after", C.c_int32),
                 ("done", C.c_int32), ("gpu_ms", C.c_double), ("preempt_signal_to_drop_us", C.c_double),
-                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("gemm_trunc_layer", C.c_int32)]
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("gemm_trunc_layer", C.c_int32),
+                ("pre_drop_layer_us", C.c_double)]
 
 
 class cs_replay_stats(C.Structure):
@@ -151,6 +159,9 @@ EXPORTS = {
     "cs_preempt_signal": ([E, C.c_uint64], C.c_int),
     "cs_iter_wait": ([E, P(cs_iter_info), P(C.c_int32), C.c_int32, P(C.c_float)], C.c_int),
     "cs_iter_poll": ([E, P(C.c_int32)], C.c_int),
+    "cs_iter_progress": ([E, P(C.c_int32)], C.c_int),
+    "cs_set_kernel_timing": ([E, C.c_int32], C.c_int),
+    "cs_kernel_timing": ([E, C.c_int32, P(cs_ktime)], C.c_int),
     "cs_debug_read_block": ([E, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "cs_debug_write_block": ([E, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "cs_debug_read_host_slot": ([E, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
@@ -164,7 +175,7 @@ EXPORTS = {
     "cs_bench_gemm": ([E, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_double), P(C.c_double),
                        P(C.c_double), P(C.c_double)], C.c_int),
     "cs_replay_run": ([E, P(C.c_int64), C.c_int64, C.c_int64, P(C.c_int64), P(C.c_double), P(C.c_double),
-                       P(C.c_int32), P(C.c_double), P(C.c_int32), P(C.c_int64), P(C.c_int64),
+                       P(C.c_int32), P(C.c_double), P(C.c_double), P(C.c_int32), P(C.c_int64), P(C.c_int64),
                        P(cs_replay_stats)], C.c_int),
     "cs_token_id": ([C.c_uint64, C.c_int64, C.c_int64, C.c_int32], C.c_int32),
     "cs_hash_uniform": ([C.c_uint64, C.c_uint64, C.c_uint64], C.c_float),

@@ -49,6 +49,7 @@ struct IterDesc {
   int32_t pad0;
   uint64_t epoch;
   uint64_t drop_ns;                            // %globaltimer at the drop
+  uint64_t start_ns;                           // %globaltimer at layer 0's head (instrumented plans)
 };
 
 // Mapped (zero-copy) host<->device record for the preemption handshake.
@@ -59,6 +60,17 @@ struct PreemptMailbox {
   volatile int32_t pad;
   volatile uint64_t seen_epoch;      // device: epoch it dropped
   volatile uint64_t seen_gpu_ns;     // device %globaltimer at the drop
+  volatile uint64_t progress;        // device: epoch * 1024 + layer the forward has entered
+};
+
+// Layer-boundary preemption check fused into the layer's first kernel
+// (add_rmsnorm): CTA 0 reads the mailbox and truncates the descriptor; the
+// kernel boundary publishes the truncation to every later launch.
+struct SafepointArg {
+  PreemptMailbox* mb;          // mapped mailbox (null: no check, no progress)
+  const __nv_bfloat16* tail;   // TP: the all-reduced vote (mode 2)
+  int32_t layer;
+  int32_t mode;                // 0 progress only, 1 host flag (g = 1), 2 agreed vote (g > 1)
 };
 
 // Prefill tile: TILE_ROWS query rows (token, head-in-group) of one entry.

@@ -41,7 +41,8 @@ void init_matrix(__nv_bfloat16* w, int64_t rows, int64_t cols, int64_t global_co
 void embed(__nv_bfloat16* x, const __nv_bfloat16* emb, const int32_t* tok_ids, int hidden, const IterDesc* desc,
            int grid, cudaStream_t s);
 void add_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16* w, __nv_bfloat16* xn, int hidden,
-                 float eps, const IterDesc* desc, const int32_t* row_idx, int grid, cudaStream_t s);
+                 float eps, const IterDesc* desc, const int32_t* row_idx, int grid, cudaStream_t s,
+                 const SafepointArg& sp = SafepointArg{});
 void silu_mul(const __nv_bfloat16* gu, __nv_bfloat16* act, int ffn, const IterDesc* desc, int grid_rows,
               cudaStream_t s);
 void rope_append(__nv_bfloat16* qkv, const int32_t* tok_pos, const int32_t* tok_slot, __nv_bfloat16* pool, int hq,
@@ -49,9 +50,7 @@ void rope_append(__nv_bfloat16* qkv, const int32_t* tok_pos, const int32_t* tok_
                  cudaStream_t s);
 void argmax_rows(const float* logits, int vocab, unsigned long long* keys, const IterDesc* desc, int grid,
                  cudaStream_t s);
-void safepoint(IterDesc* desc, PreemptMailbox* mb, int layer, cudaStream_t s);
 void safepoint_vote(__nv_bfloat16* tail, const IterDesc* desc, const PreemptMailbox* mb, cudaStream_t s);
-void safepoint_agreed(IterDesc* desc, PreemptMailbox* mb, const __nv_bfloat16* tail, int layer, cudaStream_t s);
 void read_globaltimer(uint64_t* mapped_out, cudaStream_t s);
 void calib_clock(volatile uint64_t* mb, cudaStream_t s);
 void kv_move(bool to_host, __nv_bfloat16* pool, __nv_bfloat16* host_mapped, const void* segs_mapped, int n_segs,
@@ -308,6 +307,7 @@ struct cs_engine {
     int64_t wait_h2d = 0;  // last restore writing a block this plan reads
     uint64_t signal_ns = 0;
     int64_t meta_bytes = 0;
+    double k1_bytes = 0, k2_flops = 0;  // algorithmic work per layer
   } it;
 
   void enqueue_layers();
@@ -328,6 +328,35 @@ struct cs_engine {
   }
   int gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32,
            const int32_t* m_dev = nullptr);
+  // Per-kernel-class device timing (cs_set_kernel_timing; bench roofline):
+  // event pairs on the launching stream around every non-graph launch of
+  // K8 / K2 / K1, folded into the totals at cs_iter_wait (iterations the
+  // safepoint cut are skipped: their algorithmic work is not the host's).
+  struct KTime {
+    int64_t launches = 0;
+    double ms = 0, units = 0;
+  };
+  bool ktime_on = false;
+  KTime ktime[CS_KT_N];
+  std::vector<cudaEvent_t> kt_ev;
+  std::vector<std::pair<int, double>> kt_pending;  // (class, algorithmic units) per event pair
+  template <typename Fn>
+  void timed(int cls, double units, Fn&& fn) {
+    if (!ktime_on || it.graph) {
+      fn();
+      return;
+    }
+    const size_t k = kt_pending.size();
+    while (kt_ev.size() < 2 * k + 2) {
+      cudaEvent_t ev;
+      CK(cudaEventCreate(&ev));
+      kt_ev.push_back(ev);
+    }
+    CK(cudaEventRecord(kt_ev[2 * k], s_compute));
+    fn();
+    CK(cudaEventRecord(kt_ev[2 * k + 1], s_compute));
+    kt_pending.emplace_back(cls, units);
+  }
   // K8 (csrc/gemm_pf.cu) for this layer GEMM? Prefill-sized M, or any
   // non-graph M > 256 when a safepoint may truncate the batch on the device
   bool use_pf(int M, int N, int K) const;
@@ -652,7 +681,7 @@ int cs_engine::gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int
     const CUtensorMap* xm = tmap(A, rows, K, 128);
     const CUtensorMap* wm = tmap(W, N, K, 128);
     if (xm && wm) {
-      csk::gemm_pf(xm, wm, C, M, m_dev, N, K, out_f32, sms, s_compute);
+      timed(CS_KT_K8, 2.0 * M * N * K, [&] { csk::gemm_pf(xm, wm, C, M, m_dev, N, K, out_f32, sms, s_compute); });
       return 1;
     }
   }
@@ -696,7 +725,6 @@ void cs_engine::reduce_into(__nv_bfloat16* buf, int64_t count) {
 int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   int n_launch = 0;
   const auto* desc = reinterpret_cast<const csk::IterDesc*>(d_meta);
-  auto* desc_mut = reinterpret_cast<csk::IterDesc*>(d_meta);
   // K8 GEMMs read the live row count: a safepoint drop shrinks them too
   const int32_t* m_dev = &desc->n_tok_cur;
   const bool instrumented = cfg.instrumented != 0 && it.has_offline;
@@ -710,21 +738,29 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
     if (l == 0) {
       csk::embed(x, w.emb, it.d_tok_ids, hidden, desc, T, s_compute);
     }
-    if (is_sp(l)) {
-      if (tp == 1) {
-        csk::safepoint(desc_mut, mailbox_dev, l, s_compute);
-      } else {
-        csk::safepoint_agreed(desc_mut, mailbox_dev, tail, l, s_compute);
-      }
+    // K6 rides in the layer's first kernel: progress for the host monitor at
+    // every layer of an instrumented plan, the drop check at safepoints
+    csk::SafepointArg sp{};
+    if (instrumented) {
+      sp.mb = mailbox_dev;
+      sp.layer = l;
+      sp.mode = is_sp(l) ? (tp == 1 ? 1 : 2) : 0;
+      sp.tail = tail;
     }
-    csk::add_rmsnorm(x, l == 0 ? nullptr : tmp, w.attn_norm[l], xn, hidden, cfg.rms_eps, desc, nullptr, T, s_compute);
+    csk::add_rmsnorm(x, l == 0 ? nullptr : tmp, w.attn_norm[l], xn, hidden, cfg.rms_eps, desc, nullptr, T, s_compute,
+                     sp);
     n_launch += gemm(xn, w.wqkv[l], qkv, static_cast<int>(M), qkv_cols, hidden, false, m_dev);
     csk::rope_append(qkv, it.ap.tok_pos, it.d_tok_slot, kv, hq, hkv, D, L, l,
                      cfg.rope_theta, desc, T, s_compute);
     csk::AttnParams ap = it.ap;
     ap.layer = l;
-    if (!csk::launch_attention(ap, &kv_map, D, G, graph ? Tg : it.n_dec, it.n_pt, s_compute))
-      throw ConfigError("unsupported attention shape");
+    bool ok = true;
+    const int n_dec_grid = graph ? Tg : it.n_dec;
+    if (n_dec_grid > 0)
+      timed(CS_KT_K1, it.k1_bytes, [&] { ok &= csk::launch_attention(ap, &kv_map, D, G, n_dec_grid, 0, s_compute); });
+    if (it.n_pt > 0)
+      timed(CS_KT_K2, it.k2_flops, [&] { ok &= csk::launch_attention(ap, &kv_map, D, G, 0, it.n_pt, s_compute); });
+    if (!ok) throw ConfigError("unsupported attention shape");
     {
       __nv_bfloat16* part = partial_out(tmp);
       n_launch += gemm(attn, w.wo[l], part, static_cast<int>(M), hidden, hq * D, false, m_dev);
@@ -749,7 +785,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
         }
       }
     }
-    n_launch += (l == 0 ? 1 : 0) + (is_sp(l) ? 1 : 0) + 4 + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
+    n_launch += (l == 0 ? 1 : 0) + 4 + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
                 (it.n_dec > 0 ? 1 : 0) + (it.n_pt > 0 ? (it.k2_splits > 1 ? 2 : 1) : 0);
     if ((cfg.flags & CS_FLAG_SYNC_DEBUG) && !graph) {
       CK(cudaStreamSynchronize(s_compute));
@@ -899,6 +935,15 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     }
     const int T = static_cast<int>(tok_pos.size());
     if (T > e->max_tok) throw std::invalid_argument("plan exceeds max_batched_tokens");
+    for (int i = 0; i < n; ++i) {
+      const double q = ent_qlen[i], kv = ent_kvlen[i];
+      if (ent_qlen[i] == 1) {
+        it.k1_bytes += (kv * e->hkv + e->hq) * e->D * 2.0 * 2.0;
+      } else {
+        // causal pairs of a chunk whose last query sits at kv_len - 1
+        it.k2_flops += (q * (kv - q) + q * (q + 1) / 2) * 4.0 * e->hq * e->D;
+      }
+    }
     it.n_tok = T;
     it.n_tok_on = n_tok_on;
     it.n_ent = n;
@@ -1750,6 +1795,31 @@ int cs_preempt_signal(cs_engine* e, uint64_t epoch) {
   });
 }
 
+int cs_set_kernel_timing(cs_engine* e, int32_t on) {
+  return guard([&] {
+    e->ktime_on = on != 0;
+    for (auto& t : e->ktime) t = cs_engine::KTime{};
+  });
+}
+
+int cs_kernel_timing(cs_engine* e, int32_t cls, cs_ktime* out) {
+  return guard([&] {
+    if (cls < 0 || cls >= CS_KT_N) throw std::invalid_argument("unknown kernel class");
+    out->launches = e->ktime[cls].launches;
+    out->ms = e->ktime[cls].ms;
+    out->units = e->ktime[cls].units;
+  });
+}
+
+int cs_iter_progress(cs_engine* e, int32_t* layer) {
+  return guard([&] {
+    *layer = -1;
+    if (e->host_only || e->no_model || e->dry || !e->it.active || !e->mailbox) return;
+    const uint64_t p = e->mailbox->progress;
+    if (p / 1024ull == e->it.epoch) *layer = static_cast<int32_t>(p % 1024ull);
+  });
+}
+
 int cs_iter_poll(cs_engine* e, int32_t* done) {
   return guard([&] {
     if (!e->it.active) {
@@ -1795,6 +1865,19 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
       CK(cudaEventElapsedTime(&ms, e->ev_start, e->ev_end));
       inf.gpu_ms = ms;
       const auto* desc = reinterpret_cast<const csk::IterDesc*>(e->h_out);
+      if (!e->kt_pending.empty()) {
+        if (desc->dropped_at < 0) {
+          for (size_t k = 0; k < e->kt_pending.size(); ++k) {
+            float kms = 0;
+            CK(cudaEventElapsedTime(&kms, e->kt_ev[2 * k], e->kt_ev[2 * k + 1]));
+            cs_engine::KTime& t = e->ktime[e->kt_pending[k].first];
+            t.launches += 1;
+            t.ms += kms;
+            t.units += e->kt_pending[k].second;
+          }
+        }
+        e->kt_pending.clear();
+      }
       // argmax keys: low 32 bits = ~id (0 -> -1 for rows past n_ent_cur)
       const uint64_t* keys = reinterpret_cast<const uint64_t*>(e->h_out + sizeof(csk::IterDesc));
       if (desc->dropped_at >= 0) {
@@ -1804,6 +1887,8 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
           const int64_t drop_host = static_cast<int64_t>(desc->drop_ns) - e->clock_offset_ns;
           inf.preempt_signal_to_drop_us = static_cast<double>(drop_host - static_cast<int64_t>(it.signal_ns)) / 1e3;
         }
+        if (desc->start_ns != 0 && desc->drop_ns > desc->start_ns && desc->dropped_at > 0)
+          inf.pre_drop_layer_us = static_cast<double>(desc->drop_ns - desc->start_ns) / 1e3 / desc->dropped_at;
       }
       inf.n_outputs = n_alive;
       inf.h2d_bytes = it.meta_bytes;

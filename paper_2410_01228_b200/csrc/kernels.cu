@@ -58,12 +58,52 @@ void embed(__nv_bfloat16* x, const __nv_bfloat16* emb, const int32_t* tok_ids, i
 // gathered rows row_idx[i] for i < n_ent_cur (final norm of sampled rows).
 // One CTA per row, CH 16-byte chunks per thread kept in registers: one read
 // of x (and add), one write of x and xn.
+// Truncates every *_cur count to the online prefix (online entries form a
+// prefix of the plan, scheduler.cpp:183-317) and records the layer + device
+// time in the mapped mailbox.
+__device__ __forceinline__ void apply_drop(IterDesc* desc, PreemptMailbox* mb, int layer) {
+  desc->n_tok_cur = desc->n_tok_on;
+  desc->n_ent_cur = desc->n_ent_on;
+  desc->n_dec_cur = desc->n_dec_on;
+  desc->n_pt_cur = desc->n_pt_on;
+  desc->dropped_at = layer;
+  const uint64_t now = globaltimer_ns();
+  desc->drop_ns = now;
+  mb->seen_layer = layer;
+  mb->seen_gpu_ns = now;
+  __threadfence_system();
+  mb->seen_epoch = desc->epoch;
+}
+
+// K6 at the head of layer `sp.layer` (one thread): publish progress, then if
+// the host flag carries this iteration's epoch (g = 1) or the all-reduced
+// vote is set (g > 1) and offline work remains, drop it.
+__device__ __forceinline__ void safepoint_check(IterDesc* desc, const SafepointArg& sp) {
+  if (sp.mb == nullptr) return;
+  if (sp.layer == 0) desc->start_ns = globaltimer_ns();
+  sp.mb->progress = desc->epoch * 1024ull + static_cast<uint64_t>(sp.layer);
+  if (sp.mode == 0 || desc->dropped_at >= 0) return;
+  if (sp.mode == 1) {
+    if (sp.mb->flag_epoch != desc->epoch) return;
+    if (desc->n_ent_on >= desc->n_ent_cur) return;  // nothing offline to drop
+  } else if (__bfloat162float(sp.tail[0]) <= 0.f) {
+    return;
+  }
+  apply_drop(desc, sp.mb, sp.layer);
+}
+
 template <int CH>
 __global__ void add_rmsnorm_kernel(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16* w,
                                    __nv_bfloat16* xn, int hidden, float eps, const IterDesc* desc,
-                                   const int32_t* row_idx) {
+                                   const int32_t* row_idx, SafepointArg sp) {
   pdl_trigger();  // the next projection (K7) may start streaming its weights
   const int i = blockIdx.x;
+  if (i == 0 && threadIdx.x == 0) {
+    // rows of other CTAs may see the counts before or after the drop: a
+    // dropped row's norm is never read again, the next launch sees the cut
+    safepoint_check(const_cast<IterDesc*>(desc), sp);
+  }
+  if (sp.mb != nullptr && sp.mode != 0) __syncthreads();  // CTA 0's own rows honour it
   int r;
   if (row_idx != nullptr) {
     if (i >= desc->n_ent_cur) return;
@@ -128,18 +168,19 @@ __global__ void add_rmsnorm_kernel(__nv_bfloat16* x, const __nv_bfloat16* add, c
 }
 
 void add_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16* w, __nv_bfloat16* xn, int hidden,
-                 float eps, const IterDesc* desc, const int32_t* row_idx, int grid, cudaStream_t s) {
+                 float eps, const IterDesc* desc, const int32_t* row_idx, int grid, cudaStream_t s,
+                 const SafepointArg& sp) {
   if (grid <= 0) return;
   const int vec = hidden / 8;
   // <= 512 threads: CH = ceil(vec / 512) chunks each (hidden <= 16384)
   const int threads = std::min(512, ((vec + 31) / 32) * 32);
   const int ch = (vec + threads - 1) / threads;
   if (ch == 1)
-    add_rmsnorm_kernel<1><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx);
+    add_rmsnorm_kernel<1><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx, sp);
   else if (ch == 2)
-    add_rmsnorm_kernel<2><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx);
+    add_rmsnorm_kernel<2><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx, sp);
   else
-    add_rmsnorm_kernel<4><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx);
+    add_rmsnorm_kernel<4><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx, sp);
 }
 
 // ----------------------------------------------------------------- SwiGLU ----
@@ -278,32 +319,7 @@ void argmax_rows(const float* logits, int vocab, unsigned long long* keys, const
 }
 
 // ------------------------------------------------------- safepoint (K6) ----
-// Layer-boundary check: if the host flag carries this iteration's epoch and
-// the plan still has offline work, truncate every *_cur count to the online
-// prefix (online entries form a prefix of the plan, scheduler.cpp:183-317)
-// and record the layer + device time in the mapped mailbox.
-__global__ void safepoint_kernel(IterDesc* desc, PreemptMailbox* mb, int layer) {
-  if (threadIdx.x != 0) return;
-  if (desc->dropped_at >= 0) return;
-  const uint64_t flag = mb->flag_epoch;
-  if (flag != desc->epoch) return;
-  if (desc->n_ent_on >= desc->n_ent_cur) return;  // nothing offline to drop
-  desc->n_tok_cur = desc->n_tok_on;
-  desc->n_ent_cur = desc->n_ent_on;
-  desc->n_dec_cur = desc->n_dec_on;
-  desc->n_pt_cur = desc->n_pt_on;
-  desc->dropped_at = layer;
-  const uint64_t now = globaltimer_ns();
-  desc->drop_ns = now;
-  mb->seen_layer = layer;
-  mb->seen_gpu_ns = now;
-  __threadfence_system();
-  mb->seen_epoch = desc->epoch;
-}
-
-void safepoint(IterDesc* desc, PreemptMailbox* mb, int layer, cudaStream_t s) {
-  safepoint_kernel<<<1, 32, 0, s>>>(desc, mb, layer);
-}
+// The check itself is fused into add_rmsnorm (safepoint_check above).
 
 // TP: every rank votes 1.0 into an extra element of the next all-reduce when
 // it sees the flag; after the sum every rank applies the same decision at the
@@ -318,26 +334,6 @@ __global__ void safepoint_vote_kernel(__nv_bfloat16* tail, const IterDesc* desc,
 }
 void safepoint_vote(__nv_bfloat16* tail, const IterDesc* desc, const PreemptMailbox* mb, cudaStream_t s) {
   safepoint_vote_kernel<<<1, 32, 0, s>>>(tail, desc, mb);
-}
-
-__global__ void safepoint_agreed_kernel(IterDesc* desc, PreemptMailbox* mb, const __nv_bfloat16* tail, int layer) {
-  if (threadIdx.x != 0) return;
-  if (desc->dropped_at >= 0) return;
-  if (__bfloat162float(tail[0]) <= 0.f) return;
-  desc->n_tok_cur = desc->n_tok_on;
-  desc->n_ent_cur = desc->n_ent_on;
-  desc->n_dec_cur = desc->n_dec_on;
-  desc->n_pt_cur = desc->n_pt_on;
-  desc->dropped_at = layer;
-  const uint64_t now = globaltimer_ns();
-  desc->drop_ns = now;
-  mb->seen_layer = layer;
-  mb->seen_gpu_ns = now;
-  __threadfence_system();
-  mb->seen_epoch = desc->epoch;
-}
-void safepoint_agreed(IterDesc* desc, PreemptMailbox* mb, const __nv_bfloat16* tail, int layer, cudaStream_t s) {
-  safepoint_agreed_kernel<<<1, 32, 0, s>>>(desc, mb, tail, layer);
 }
 
 // Clock calibration: spin until the host stores its CLOCK_MONOTONIC into the

@@ -55,7 +55,8 @@ double now_ms() {
 
 extern "C" int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin, int64_t op_end,
                              const int64_t* plans, double* gpu_ms, double* wall_end_ms, int32_t* dropped_layer,
-                             double* drop_latency_us, int32_t* gemm_trunc_layer, int64_t* h2d_bytes,
+                             double* drop_latency_us, double* pre_drop_layer_us, int32_t* gemm_trunc_layer,
+                             int64_t* h2d_bytes,
                              int64_t* d2h_bytes, cs_replay_stats* st) {
   std::memset(st, 0, sizeof(*st));
   st->first_mismatch_op = -1;
@@ -67,6 +68,7 @@ extern "C" int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin,
   std::vector<cs_batch_entry> entries;
   std::set<int64_t> live;  // registered, not released (as the recorder tracks them)
   bool inflight = false, signal_armed = false;
+  int32_t signal_layer = 0;  // the reference's drop layer of the in-flight iteration
   int64_t it = 0;
   const double t0 = now_ms();
   for (int64_t i = op_begin; i < op_end; ++i) {
@@ -148,12 +150,28 @@ extern "C" int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin,
         ++epoch;
         rc = cs_forward_launch(e, entries.data(), static_cast<int32_t>(n), epoch);
         inflight = rc == CS_OK;
-        signal_armed = o[3] != 0;  // the reference dropped offline work this iteration
+        // o[3] = 1 + the layer at which the reference dropped offline work
+        // this iteration (0: no drop)
+        signal_armed = o[3] != 0;
+        signal_layer = static_cast<int32_t>(o[3] - 1);
         break;
       }
       case kSignal:
         if (inflight && signal_armed) {
-          rc = cs_preempt_signal(e, epoch);
+          // Alg. 1 fired while the reference's forward was in layer
+          // signal_layer - 1 (its drop took effect at the next safepoint,
+          // preemption.cpp:95-114): store the flag once the device has
+          // entered that layer, so the drop lands where the reference's did
+          // and flag -> drop is the real one-safepoint latency.
+          const double w0 = now_ms();
+          for (;;) {
+            int32_t at = -1, done = 0;
+            rc = cs_iter_progress(e, &at);
+            if (rc != CS_OK || at >= signal_layer - 1) break;
+            rc = cs_iter_poll(e, &done);
+            if (rc != CS_OK || done || now_ms() - w0 > 5000.0) break;
+          }
+          if (rc == CS_OK) rc = cs_preempt_signal(e, epoch);
           signal_armed = false;
         }
         break;
@@ -167,6 +185,7 @@ extern "C" int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin,
           if (wall_end_ms) wall_end_ms[it] = now_ms() - t0;
           if (dropped_layer) dropped_layer[it] = info.preempted_at_layer;
           if (drop_latency_us) drop_latency_us[it] = info.preempt_signal_to_drop_us;
+          if (pre_drop_layer_us) pre_drop_layer_us[it] = info.pre_drop_layer_us;
           if (gemm_trunc_layer) gemm_trunc_layer[it] = info.gemm_trunc_layer;
           if (h2d_bytes) h2d_bytes[it] = info.h2d_bytes;
           if (d2h_bytes) d2h_bytes[it] = info.d2h_bytes;

@@ -374,6 +374,21 @@ class Engine(KvPool):
         _check(_lib.cs_iter_poll(self._h, C.byref(d)))
         return bool(d.value)
 
+    def iter_progress(self) -> int:
+        """Layer the in-flight instrumented forward has entered (-1: none)."""
+        v = C.c_int32()
+        _check(_lib.cs_iter_progress(self._h, C.byref(v)))
+        return int(v.value)
+
+    def set_kernel_timing(self, on: bool) -> None:
+        _check(_lib.cs_set_kernel_timing(self._h, 1 if on else 0))
+
+    def kernel_timing(self, cls: int) -> F.cs_ktime:
+        """(launches, ms, algorithmic units) of one kernel class (CS_KT_*)."""
+        t = F.cs_ktime()
+        _check(_lib.cs_kernel_timing(self._h, cls, C.byref(t)))
+        return t
+
     def iter_wait(self, want_logits: bool = False):
         info = F.cs_iter_info()
         cap = 4096

@@ -118,9 +118,10 @@ def load(calls_path: str, requests_path: Optional[str] = None) -> Trace:
             ops.append(r)
     ops_a = np.array(ops, dtype=np.int64).reshape(-1, 8)
     disp = np.nonzero(ops_a[:, 0] == OPC["dispatch"])[0]
-    # arm the preemption signal only for iterations the reference dropped
+    # arm the preemption signal only for iterations the reference dropped,
+    # with the layer it dropped at (1 + layer; 0 = no drop)
     for k, i in enumerate(disp):
-        ops_a[i, 3] = 1 if dropped[k] >= 0 else 0
+        ops_a[i, 3] = 1 + dropped[k] if dropped[k] >= 0 else 0
     bounds = np.concatenate([[0], disp[1:], [len(ops_a)]]).astype(np.int64)
     tr = Trace(config, ops_a, np.array(plans, dtype=np.int64).reshape(-1, 5), bounds, plan_of, end_plan_of,
                np.array(end_now, dtype=np.int64), np.array(dropped, dtype=np.int32), audit=audit)
@@ -143,6 +144,7 @@ class WindowResult:
     wall_end_ms: np.ndarray
     dropped_layer: np.ndarray
     drop_latency_us: np.ndarray
+    pre_drop_layer_us: np.ndarray
     gemm_trunc_layer: np.ndarray
     h2d_bytes: np.ndarray
     d2h_bytes: np.ndarray
@@ -155,7 +157,7 @@ def run(eng: Engine, tr: Trace, it_begin: int, it_end: int, dry: bool = False,
     with the reference's digest at every build (host work: off in benches)."""
     n = it_end - it_begin
     arrs = dict(gpu_ms=np.zeros(n), wall_end_ms=np.zeros(n), dropped_layer=np.full(n, -1, np.int32),
-                drop_latency_us=np.zeros(n), gemm_trunc_layer=np.full(n, -1, np.int32),
+                drop_latency_us=np.zeros(n), pre_drop_layer_us=np.zeros(n), gemm_trunc_layer=np.full(n, -1, np.int32),
                 h2d_bytes=np.zeros(n, np.int64), d2h_bytes=np.zeros(n, np.int64))
     ptr = {k: v.ctypes.data_as(C.POINTER({np.float64: C.c_double, np.int32: C.c_int32,
                                           np.int64: C.c_int64}[v.dtype.type])) for k, v in arrs.items()}
@@ -167,7 +169,7 @@ def run(eng: Engine, tr: Trace, it_begin: int, it_end: int, dry: bool = False,
     rc = lib().cs_replay_run(eng._h, ops.ctypes.data_as(C.POINTER(C.c_int64)), int(tr.bounds[it_begin]),
                              int(tr.bounds[it_end]), plans.ctypes.data_as(C.POINTER(C.c_int64)),
                              ptr["gpu_ms"], ptr["wall_end_ms"], ptr["dropped_layer"], ptr["drop_latency_us"],
-                             ptr["gemm_trunc_layer"], ptr["h2d_bytes"], ptr["d2h_bytes"], C.byref(st))
+                             ptr["pre_drop_layer_us"], ptr["gemm_trunc_layer"], ptr["h2d_bytes"], ptr["d2h_bytes"], C.byref(st))
     if rc != F.CS_OK:
         msg = lib().cs_last_error().decode()
         raise RuntimeError(f"replay failed at op {st.first_mismatch_op} "

@@ -30,6 +30,28 @@ def test_reference_arm_prints_one_contract_line():
     assert "workload" in d["config"] and cb["sample"]
 
 
+def test_reference_arm_never_loads_the_product():
+    """The reference arm times the CPU port and the reference's own control
+    plane only: the product package (and its .so) must stay unloaded."""
+    code = ("import sys, bench, argparse; "
+            "bench.run_reference(argparse.Namespace(workload='llama8b', warmup=0, steps=1, gpus=1, replicas=False)); "
+            "bad = [m for m in sys.modules if m.startswith('paper_2410_01228_b200')]; "
+            "maps = open('/proc/self/maps').read(); "
+            "assert not bad and 'libconserve_b200' not in maps, (bad,)")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_step_slices_cover_the_run():
+    sys.path.insert(0, ROOT)
+    import bench
+    W, sl = bench.slices(1375, 5, 20)
+    assert W == 5 and len(sl) == 20 and sl[0][0] == 5 and sl[-1][1] == 1375
+    assert all(a < b for a, b in sl) and all(sl[i][1] == sl[i + 1][0] for i in range(19))
+    W, sl = bench.slices(10, 3, 50)
+    assert W == 3 and len(sl) == 7 and sl[-1][1] == 10
+
+
 def test_percentile_is_nearest_rank():
     sys.path.insert(0, ROOT)
     import bench
