@@ -261,6 +261,15 @@ int cs_iter_poll(cs_engine* e, int32_t* done);
  * monitor time its flag store against the device's layer clock
  * (IterationExecution::safepoint_time, preemption.cpp:74-82). */
 int cs_iter_progress(cs_engine* e, int32_t* layer);
+/* Device time of the in-flight forward once it completed (*ms = -1 while it
+ * runs; bookkeeping-only engines report -1). Does not end the iteration. */
+int cs_iter_elapsed(cs_engine* e, double* ms);
+/* Live mode (oracle/lockstep/live.cpp): the host's event loop decided the
+ * in-flight iteration drops its offline entries at `layer`
+ * (IterationExecution::apply_drop, preemption.cpp:105-114) after the device
+ * already ran the whole plan. cs_iter_wait then treats it as dropped: only
+ * the online prefix produces outputs and records written KV. */
+int cs_iter_retro_drop(cs_engine* e, int32_t layer);
 
 /* Per-kernel-class device timing for the roofline (bench): while enabled,
  * every non-graph launch of a class is bracketed by CUDA events on its

@@ -89,10 +89,27 @@ struct EngineDeleter {
 };
 }  // namespace detail
 
+/* Process-wide data-plane model for managers the reference constructs itself
+ * (SimEngine builds `KvCacheManager(cluster, incremental)`, sim_engine.cpp):
+ * set it before constructing the engine and those managers own a real device
+ * engine of that shape (device, sharding, flags) instead of bookkeeping only.
+ * last_engine() is the handle of the most recently opened one, for the
+ * forward seam (cs_forward_launch) -- the live-mode host. */
+inline const cs_config*& data_plane_model() {
+  static const cs_config* m = nullptr;
+  return m;
+}
+inline cs_engine*& last_engine() {
+  static cs_engine* e = nullptr;
+  return e;
+}
+
 class KvCacheManager {
  public:
   KvCacheManager() = default;
-  KvCacheManager(const coserve::ClusterConfig& cluster, bool incremental) { open(cluster, incremental, nullptr); }
+  KvCacheManager(const coserve::ClusterConfig& cluster, bool incremental) {
+    open(cluster, incremental, data_plane_model());
+  }
   KvCacheManager(const coserve::ClusterConfig& cluster, bool incremental, const cs_config& model) {
     open(cluster, incremental, &model);
   }
@@ -232,6 +249,7 @@ class KvCacheManager {
     cs_engine* e = nullptr;
     detail::check(cs_create(&cfg, &e));
     e_ = std::shared_ptr<cs_engine>(e, detail::EngineDeleter{});
+    last_engine() = e;
   }
   cs_engine* h() const {
     if (!e_) throw std::logic_error("KvCacheManager: default-constructed (no engine)");

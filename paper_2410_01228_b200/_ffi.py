@@ -160,6 +160,8 @@ EXPORTS = {
     "cs_iter_wait": ([E, P(cs_iter_info), P(C.c_int32), C.c_int32, P(C.c_float)], C.c_int),
     "cs_iter_poll": ([E, P(C.c_int32)], C.c_int),
     "cs_iter_progress": ([E, P(C.c_int32)], C.c_int),
+    "cs_iter_elapsed": ([E, P(C.c_double)], C.c_int),
+    "cs_iter_retro_drop": ([E, C.c_int32], C.c_int),
     "cs_set_kernel_timing": ([E, C.c_int32], C.c_int),
     "cs_kernel_timing": ([E, C.c_int32, P(cs_ktime)], C.c_int),
     "cs_debug_read_block": ([E, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),

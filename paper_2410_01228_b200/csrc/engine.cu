@@ -308,6 +308,7 @@ struct cs_engine {
     uint64_t signal_ns = 0;
     int64_t meta_bytes = 0;
     double k1_bytes = 0, k2_flops = 0;  // algorithmic work per layer
+    int32_t retro_layer = -1;  // host-decided drop after the device finished (cs_iter_retro_drop)
   } it;
 
   void enqueue_layers();
@@ -1811,6 +1812,28 @@ int cs_kernel_timing(cs_engine* e, int32_t cls, cs_ktime* out) {
   });
 }
 
+int cs_iter_elapsed(cs_engine* e, double* ms) {
+  return guard([&] {
+    *ms = -1;
+    if (!e->it.active) throw std::logic_error("no iteration in flight");
+    if (e->host_only || e->no_model || e->dry) return;
+    const cudaError_t q = cudaEventQuery(e->ev_end);
+    if (q == cudaErrorNotReady) return;
+    CK(q);
+    float v = 0;
+    CK(cudaEventElapsedTime(&v, e->ev_start, e->ev_end));
+    *ms = v;
+  });
+}
+
+int cs_iter_retro_drop(cs_engine* e, int32_t layer) {
+  return guard([&] {
+    if (!e->it.active) throw std::logic_error("no iteration in flight");
+    if (layer < 1) throw std::invalid_argument("drop layer must be >= 1");
+    e->it.retro_layer = layer;
+  });
+}
+
 int cs_iter_progress(cs_engine* e, int32_t* layer) {
   return guard([&] {
     *layer = -1;
@@ -1890,6 +1913,10 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
         if (desc->start_ns != 0 && desc->drop_ns > desc->start_ns && desc->dropped_at > 0)
           inf.pre_drop_layer_us = static_cast<double>(desc->drop_ns - desc->start_ns) / 1e3 / desc->dropped_at;
       }
+      if (desc->dropped_at < 0 && it.retro_layer >= 0) {
+        inf.preempted_at_layer = it.retro_layer;
+        n_alive = it.n_ent_on;
+      }
       inf.n_outputs = n_alive;
       inf.h2d_bytes = it.meta_bytes;
       inf.d2h_bytes = static_cast<int64_t>(sizeof(csk::IterDesc) + sizeof(uint64_t) * (it.graph ? it.bucket : it.n_ent));
@@ -1902,6 +1929,10 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
       if (logits && n_alive > 0)
         CK(cudaMemcpy(logits, e->logits, static_cast<size_t>(n_alive) * e->vocab * 4, cudaMemcpyDeviceToHost));
     } else {
+      if (it.retro_layer >= 0) {
+        inf.preempted_at_layer = it.retro_layer;
+        n_alive = it.n_ent_on;
+      }
       inf.n_outputs = n_alive;
     }
     inf.n_entries_after = n_alive;
