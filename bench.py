@@ -434,6 +434,46 @@ def safepoint_overhead(cs, F, reps=8):
             e.close()
 
 
+def live_leg(name, device, margin=None):
+    """Live mode (oracle/lockstep/live.cpp): the UNMODIFIED reference SimEngine
+    schedules on its fit, but its clock advances by the measured device time
+    of each real forward on this GPU (KV calls on the HBM pool). Returns the
+    reference's own metrics.json of that run (offline tok/s at its measured
+    TBT) plus the tool's summary."""
+    import tempfile
+    exe = os.path.join(ROOT, "oracle", "_ref", "adapter", "live")
+    if not os.path.exists(exe):
+        return {"unavailable": "oracle/_ref/adapter/live not built (make -C oracle live)"}
+    trace, preset, _ = WORKLOADS[name]
+    g = os.path.join(ROOT, "tests", "golden", trace)
+    c = json.load(open(os.path.join(g, "run_config.json")))
+    wl = c.get("workload", {})
+    if isinstance(wl.get("trace"), str):
+        wl["trace"] = os.path.join(g, wl["trace"])
+    if margin is not None:
+        c.setdefault("slo", {})["safety_margin"] = margin
+    with tempfile.TemporaryDirectory() as tmp:
+        cp = os.path.join(tmp, "run_config.json")
+        json.dump(c, open(cp, "w"))
+        try:
+            r = subprocess.run([exe, cp, tmp, preset, "--device", str(device)], capture_output=True, text=True,
+                               timeout=900)
+        except Exception as ex:
+            return {"error": str(ex)}
+        if r.returncode != 0:
+            return {"error": r.stderr[-500:]}
+        summ = json.loads(r.stdout.strip().splitlines()[-1])
+        m = json.load(open(os.path.join(tmp, "metrics.json")))
+    slo = c.get("slo", {})
+    return {"offline_tok_s": m["offline_throughput"], "online_p99_tbt_ms": 1e3 * m["tbt"]["p99"],
+            "online_p99_ttft_ms": 1e3 * m["ttft"]["p99"], "tbt_attainment": m["tbt_attainment"],
+            "ttft_attainment": m["ttft_attainment"], "slo_tbt_ms": 1e3 * slo.get("tbt_slo_s", 0.1),
+            "slo_ttft_ms": 1e3 * slo.get("ttft_slo_s", 0.5), "safety_margin": slo.get("safety_margin", 0.05),
+            "preemptions": m["preemptions"], "iterations": summ["iterations"], "horizon_s": m["horizon_s"],
+            "measured_over_predicted_median": summ["measured_over_predicted_median"],
+            "transferred_bytes": m["transferred_bytes"], "wall_s": summ["wall_s"]}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -511,7 +551,7 @@ def main():
             dist.barrier()
         clocks = sampler.stop()
         s1 = eng.stats()
-        kt = {c: eng.kernel_timing(c) for c in (F.CS_KT_K8, F.CS_KT_K2, F.CS_KT_K1)}
+        kt = {c: eng.kernel_timing(c) for c in (F.CS_KT_K8, F.CS_KT_K2, F.CS_KT_K1, F.CS_KT_LIB, F.CS_KT_GRAPH)}
         eng.set_kernel_timing(False)
         for p in parts:
             assert p.mismatches == 0, f"replay diverged from the reference at op {p.first_mismatch_op}"
@@ -561,6 +601,11 @@ def main():
                          "offline_tokens": o["off"], "iterations": o["iters"], "d2h_bytes": d2h_b,
                          "h2d_bytes": h2d_b, "drops": int((o["dropped"] >= 0).sum())}
 
+    live = {}
+    if not args.no_probes and rank == 0 and world == 1:
+        live["recorded_margin"] = live_leg(args.workload, local)
+        live["margin_0"] = live_leg(args.workload, local, margin=0.0)
+
     probes = {}
     if not args.no_probes and rank == 0:
         probes["attention"] = attention_probe(cs, F, hbm_peak, bf16_peak)
@@ -603,12 +648,23 @@ def main():
                        "algorithmic_per_launch": per,
                        "share_of_window": t.ms / (gpu_s * 1e3)}
     dom = max(kinfo, key=lambda k: kinfo[k]["ms_total"]) if kinfo else None
+    # where the rest of the window goes: library GEMMs of non-graph forwards,
+    # whole decode-graph forwards (cuBLAS GEMMs + K1 + norms inside)
+    lib, gr = rp["kt"][F.CS_KT_LIB], rp["kt"][F.CS_KT_GRAPH]
+    breakdown = {k: v["share_of_window"] for k, v in kinfo.items()}
+    breakdown["cublas_gemm_nongraph"] = lib.ms / (gpu_s * 1e3)
+    breakdown["cublas_gemm_nongraph_tflops"] = lib.units / (lib.ms * 1e-3) / 1e12 if lib.ms > 0 else None
+    breakdown["decode_graph_forwards"] = gr.ms / (gpu_s * 1e3)
+    breakdown["decode_graph_iterations"] = int(gr.launches)
+    breakdown["other"] = 1.0 - sum(v for k, v in breakdown.items()
+                                   if k in kinfo or k in ("cublas_gemm_nongraph", "decode_graph_forwards"))
     roofline = dict(kinfo[dom]) if dom else {}
     if dom:
         roofline["peak_kind"] = peak_kind
         roofline["others"] = {k: {x: v[x] for x in ("achieved", "unit", "frac", "share_of_window", "launches")}
                               for k, v in kinfo.items() if k != dom}
         roofline["probes"] = probes.get("attention")
+        roofline["window_breakdown"] = breakdown
 
     dl = rp["dropped"]
     drops = []
@@ -661,6 +717,10 @@ def main():
                     "frac_h2d": (h2d_b / (h2d_ms * 1e-3) / 1e9) / link_peak["h2d"] if h2d_ms > 0 else None},
         "nonresident_reads": s1.nonresident_reads,
         "legs": legs,
+        "live": dict(live, what="live mode (oracle/lockstep/live.cpp): the unmodified reference SimEngine schedules "
+                                "on its B200 fit while its clock advances by the measured device time of each "
+                                "real forward on this GPU; metrics are the reference's own metrics.json") if live
+        else None,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": rp["clocks"],

@@ -206,6 +206,8 @@ typedef struct {
   int64_t nonresident_reads;     /* block-table reads of pages the reference marks non-resident (D3) */
   double moved_d2h_ms, moved_h2d_ms;  /* summed device time of the gather / scatter kernels */
   int64_t kernel_launches;       /* hand-written kernels launched so far (cuBLAS/NCCL excluded) */
+  int64_t host_lru_evicted_pages; /* host copies dropped by the host LRU (kv_cache.cpp:326-362) */
+  int64_t unbacked_reads;        /* block-table reads past a request's pages (reference defect D5) */
 } cs_kv_stats;
 int cs_kv_stats_get(cs_engine* e, cs_kv_stats* out);
 int cs_kv_request_info(cs_engine* e, int64_t id, int64_t* gpu_pages, int64_t* covered_tokens,
@@ -275,9 +277,11 @@ int cs_iter_retro_drop(cs_engine* e, int32_t layer);
  * every non-graph launch of a class is bracketed by CUDA events on its
  * stream; totals cover iterations that completed without a drop.
  * units = algorithmic work of the timed launches: flops for
- * K8 (2*M*N*K) and K2 (4*Hq*d per causal query-key pair), bytes for K1
- * (K/V read + Q/O). Enabling resets the totals. */
-enum { CS_KT_K8 = 0, CS_KT_K2 = 1, CS_KT_K1 = 2, CS_KT_N = 3 };
+ * K8 (2*M*N*K), K2 (4*Hq*d per causal query-key pair) and the library
+ * (cuBLAS) GEMMs of non-graph forwards (CS_KT_LIB), bytes for K1 (K/V read
+ * + Q/O); CS_KT_GRAPH counts whole decode-graph forwards (units = token
+ * rows). Enabling resets the totals. */
+enum { CS_KT_K8 = 0, CS_KT_K2 = 1, CS_KT_K1 = 2, CS_KT_LIB = 3, CS_KT_GRAPH = 4, CS_KT_N = 5 };
 typedef struct {
   int64_t launches;
   double ms;

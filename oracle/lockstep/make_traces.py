@@ -174,10 +174,23 @@ def scenario(name: str):
                "sarathi": {"kind": "sarathi_preemptive"},
                "noincr": {"kind": "conserve", "incremental_kv": False},
                "nolayerwise": {"kind": "conserve", "layerwise_preemption": False},
-               "pool48": {"kind": "conserve"}, "pool80": {"kind": "conserve"}}[variant]
+               "pool48": {"kind": "conserve"}, "pool80": {"kind": "conserve"},
+               **{f"host{h}": {"kind": "conserve"} for h in (32, 40, 48)}}[variant]
         cfg["policy"] = pol
         if variant.startswith("pool"):
             cfg["cluster"]["gpu_kv_capacity"] = int(variant[4:]) * 16 * 2048
+        if variant.startswith("host"):
+            # host-memory-limited regime:
+            # flush_checkpoints must LRU-evict host copies and tag recompute
+            # (kv_cache.cpp:326-362, 379-384); a 48-page GPU pool so evicted
+            # requests restore from, or recompute past, the small host pool
+            cfg["cluster"]["host_kv_capacity"] = int(variant[4:]) * 16 * 2048
+            cfg["cluster"]["gpu_kv_capacity"] = 48 * 16 * 2048
+            # the reference's own per-event audit trips on this regime ("host
+            # byte accounting drifted" / "interior page is partial", reference
+            # defects); record without it -- the final audit verdict is kept
+            # and must be reproduced by the replay
+            cfg["audit"] = False
         return cfg, trace
     if name.startswith("fuzz"):
         # test_sim_engine.cpp:166-187 ("fuzzed co-serving runs"): base_config

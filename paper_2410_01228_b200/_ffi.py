@@ -85,6 +85,7 @@ class cs_kv_stats(C.Structure):
         ("quarantined_blocks", C.c_int64), ("n_host_slots", C.c_int64), ("free_host_slots", C.c_int64),
         ("moved_d2h_bytes", C.c_int64), ("moved_h2d_bytes", C.c_int64), ("nonresident_reads", C.c_int64),
         ("moved_d2h_ms", C.c_double), ("moved_h2d_ms", C.c_double), ("kernel_launches", C.c_int64),
+        ("host_lru_evicted_pages", C.c_int64), ("unbacked_reads", C.c_int64),
     ]
 
 
@@ -97,7 +98,7 @@ class cs_ktime(C.Structure):
     _fields_ = [("launches", C.c_int64), ("ms", C.c_double), ("units", C.c_double)]
 
 
-CS_KT_K8, CS_KT_K2, CS_KT_K1 = 0, 1, 2
+CS_KT_K8, CS_KT_K2, CS_KT_K1, CS_KT_LIB, CS_KT_GRAPH = 0, 1, 2, 3, 4
 
 
 class cs_iter_info(C.Structure):

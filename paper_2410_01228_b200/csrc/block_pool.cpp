@@ -190,7 +190,14 @@ void BlockPool::note_written(int64_t id, int64_t w0, int64_t w1) {
 
 int32_t BlockPool::block_for_read(int64_t id, size_t page_idx) {
   Req& r = req(id);
-  if (page_idx >= r.pages.size()) throw LogicError("attention reads past the request's pages");
+  if (page_idx >= r.pages.size()) {
+    // The reference dispatched an entry over positions it holds no pages for
+    // (host-limited regime: a prefill continuation of a request whose context
+    // release_offline_pages_on_demand discarded in the same build, DESIGN.md
+    // D5). Those rows read and write the scratch block, never a live one.
+    ++unbacked_reads_;
+    return scratch_block();
+  }
   Page& p = r.pages[page_idx];
   if (p.on_gpu && !p.discarded && p.block >= 0) return p.block;
   // The reference dispatched a plan whose context is not GPU-resident (D3).
@@ -442,7 +449,10 @@ void BlockPool::stage_checkpoint(int64_t id, int64_t from_token, int64_t to_toke
   Req& r = req(id);
   const int64_t pt = cfg_.page_tokens;
   for (int64_t pi = from_token / pt; pi <= (to_token - 1) / pt; ++pi) {
-    if (pi >= static_cast<int64_t>(r.pages.size())) throw LogicError("checkpoint range past coverage");
+    // The reference indexes r.pages[page_idx] unchecked here (kv_cache.cpp:
+    // 315, undefined behaviour past the vector) when it stages the range of
+    // an entry it dispatched without pages (D5); there is nothing to copy.
+    if (pi >= static_cast<int64_t>(r.pages.size())) break;
     Page& p = r.pages[static_cast<size_t>(pi)];
     if (p.discarded || !p.on_gpu) continue;
     const int64_t target = std::min(p.tokens, to_token - pi * pt);
@@ -485,6 +495,7 @@ int64_t BlockPool::evict_host_bytes(int64_t needed) {
       continue;
     }
     freed += p.host_tokens * bpt;
+    ++host_lru_evicted_;
     host_used_ -= p.host_tokens * bpt;
     p.host_tokens = 0;
     retire_slot(p);

@@ -171,6 +171,11 @@ class BlockPool {
   int64_t total_d2h() const { return total_d2h_; }
   int64_t total_h2d() const { return total_h2d_; }
   int64_t recompute_tagged() const { return recompute_tagged_; }
+  int64_t host_lru_evicted() const { return host_lru_evicted_; }
+  int64_t unbacked_reads() const { return unbacked_reads_; }
+  // one device block past the pool, never allocated: target of rows the
+  // reference dispatched without pages (block_for_read)
+  int32_t scratch_block() const { return static_cast<int32_t>(cfg_.n_blocks); }
   bool transfers_inflight() const { return !jobs_.empty(); }
   // Device ordinal of a reference job (dir, ordinal); ordinal 0 when it moved
   // nothing on the device. Known for every job id issued so far.
@@ -239,6 +244,7 @@ class BlockPool {
   int64_t next_job_ = 1;
   int64_t gpu_used_ = 0, host_used_ = 0;
   int64_t total_d2h_ = 0, total_h2d_ = 0, recompute_tagged_ = 0;
+  int64_t host_lru_evicted_ = 0, unbacked_reads_ = 0;
   uint64_t host_stamp_ = 0;
   std::map<uint64_t, std::pair<int64_t, size_t>> host_lru_;  // stamp -> (req, page)
 

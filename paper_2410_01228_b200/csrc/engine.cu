@@ -687,10 +687,12 @@ int cs_engine::gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int
     }
   }
   if (wgemm(A, W, C, M, N, K, out_f32)) return 1;
-  if (lt_gemm(A, W, C, M, N, K, out_f32)) return 0;
-  const float alpha = 1.f, beta = 0.f;
-  CKB(cublasGemmEx(blas, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, W, CUDA_R_16BF, K, A, CUDA_R_16BF, K, &beta, C,
-                   out_f32 ? CUDA_R_32F : CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
+  timed(CS_KT_LIB, 2.0 * M * N * K, [&] {
+    if (lt_gemm(A, W, C, M, N, K, out_f32)) return;
+    const float alpha = 1.f, beta = 0.f;
+    CKB(cublasGemmEx(blas, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, W, CUDA_R_16BF, K, A, CUDA_R_16BF, K, &beta, C,
+                     out_f32 ? CUDA_R_32F : CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
+  });
   return 0;
 }
 
@@ -1219,9 +1221,10 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
       CK(cudaEventCreateWithFlags(&e->ev_fwd_done, cudaEventDisableTiming));
 
       const size_t blk_bytes = static_cast<size_t>(e->block_elems) * 2;
-      CK(cudaMalloc(&e->kv, static_cast<size_t>(pc.n_blocks) * blk_bytes));
-      CK(cudaMemset(e->kv, 0, static_cast<size_t>(pc.n_blocks) * blk_bytes));  // finite everywhere
-      make_kv_tensor_map(&e->kv_map, e->kv, static_cast<uint64_t>(pc.n_blocks) * e->L * 2 * e->hkv * 16, e->D);
+      // + 1: the scratch block (BlockPool::scratch_block)
+      CK(cudaMalloc(&e->kv, static_cast<size_t>(pc.n_blocks + 1) * blk_bytes));
+      CK(cudaMemset(e->kv, 0, static_cast<size_t>(pc.n_blocks + 1) * blk_bytes));  // finite everywhere
+      make_kv_tensor_map(&e->kv_map, e->kv, static_cast<uint64_t>(pc.n_blocks + 1) * e->L * 2 * e->hkv * 16, e->D);
       CK(cudaHostAlloc(&e->host_kv, static_cast<size_t>(pc.n_slots) * blk_bytes,
                        cudaHostAllocMapped | cudaHostAllocPortable));
       CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->host_kv_dev), e->host_kv, 0));
@@ -1629,6 +1632,8 @@ int cs_kv_stats_get(cs_engine* e, cs_kv_stats* o) {
     o->moved_d2h_bytes = p.moved_d2h();
     o->moved_h2d_bytes = p.moved_h2d();
     o->nonresident_reads = p.nonresident_reads();
+    o->host_lru_evicted_pages = p.host_lru_evicted();
+    o->unbacked_reads = p.unbacked_reads();
     o->moved_d2h_ms = e->moved_ms[CS_D2H];
     o->kernel_launches = e->launches.load();
     o->moved_h2d_ms = e->moved_ms[CS_H2D];
@@ -1888,6 +1893,12 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
       CK(cudaEventElapsedTime(&ms, e->ev_start, e->ev_end));
       inf.gpu_ms = ms;
       const auto* desc = reinterpret_cast<const csk::IterDesc*>(e->h_out);
+      if (e->ktime_on && it.graph && desc->dropped_at < 0) {
+        cs_engine::KTime& t = e->ktime[CS_KT_GRAPH];
+        t.launches += 1;
+        t.ms += ms;
+        t.units += it.n_tok;
+      }
       if (!e->kt_pending.empty()) {
         if (desc->dropped_at < 0) {
           for (size_t k = 0; k < e->kt_pending.size(); ++k) {

@@ -104,7 +104,8 @@ def _replay_with_oracle(name):
 
 
 @pytest.mark.parametrize("name", ["config1", "config1_pool48", "config1_pool80", "config1_nolayerwise",
-                                  "config1_noincr", "config1_nonpreemptive", "config1_onlineonly", "config1_sarathi"])
+                                  "config1_noincr", "config1_nonpreemptive", "config1_onlineonly", "config1_sarathi",
+                                  "config1_host40", "config1_host48"])
 def test_reference_run_logits_match_oracle(name):
     iters, worst, agree, drops, st = _replay_with_oracle(name)
     assert iters >= 15

@@ -18,10 +18,20 @@ def _cfg():
                            safepoint_interval_layers=1, instrumented=1)
 
 
+def _cfg_slow():
+    # a forward long enough (~2 ms of GEMMs) that the host's flag store after
+    # cs_forward_launch returns lands before the last layer: with the check
+    # fused into the layer-head kernel, an 8-layer hidden-512 forward is
+    # enqueue-bound and may already be in its last layer when launch returns
+    return cs.model_config("tiny", num_layers=8, hidden=1024, n_heads=16, n_kv_heads=8, head_dim=64, ffn=4096,
+                           vocab=512, max_batched_tokens=8192, gpu_kv_capacity=16384 * 2 * 8 * 8 * 64 * 2,
+                           safepoint_interval_layers=1, instrumented=1)
+
+
 def test_flag_drops_offline_and_keeps_online_exact():
-    drv = Driver(_cfg())
+    drv = Driver(_cfg_slow())
     drv.add(0, 30, online=True)
-    drv.add(1, 3000, online=False)
+    drv.add(1, 6000, online=False)
     info, lg, ref = drv.step([(0, None), (1, None)], preempt_after_launch=True)
     assert info.preempted_at_layer is not None and 1 <= info.preempted_at_layer < 8
     assert info.n_outputs == 1
