@@ -55,6 +55,8 @@ void read_globaltimer(uint64_t* mapped_out, cudaStream_t s);
 void calib_clock(volatile uint64_t* mb, cudaStream_t s);
 void kv_move(bool to_host, __nv_bfloat16* pool, __nv_bfloat16* host_mapped, const void* segs_mapped, int n_segs,
              int runs_per_seg, int D, int sms, cudaStream_t s);
+void kv_pack(bool to_stage, __nv_bfloat16* pool, __nv_bfloat16* stage, const void* segs, const int64_t* stage_off,
+             int n_segs, int runs_per_seg, int D, int sms, cudaStream_t s);
 void fill_pool(__nv_bfloat16* pool, size_t n, uint64_t seed, cudaStream_t s);
 bool launch_attention(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_dec_grid,
                       int n_pt_grid, cudaStream_t s);
@@ -284,6 +286,11 @@ struct cs_engine {
   bool wgemm_launch(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
   ncclComm_t comm = nullptr;
   DescRing ring[2];
+  // K4/K5 DMA path: per-direction device staging (token-major, like a host
+  // slot) between the pack/unpack kernel and the copy-engine transfer
+  __nv_bfloat16* stage[2] = {nullptr, nullptr};
+  size_t stage_elems = 0;
+  bool kv_zerocopy = false;  // CS_KV_ZEROCOPY=1: SM zero-copy kernel instead (A/B)
   double moved_ms[2] = {0, 0};
   std::atomic<int64_t> launches{0};  // hand-written kernel launches (not cuBLAS/NCCL)
 
@@ -391,10 +398,6 @@ namespace {
 int64_t DeviceMover::launch(int dir, const std::vector<csb::Segment>& segs, int64_t after_other) {
   if (e->dry || segs.empty()) return 0;
   auto ev = std::make_shared<EventPair>();
-  const size_t n = segs.size() * sizeof(csb::Segment);
-  DescRing& ring = e->ring[dir];
-  const size_t off = ring.alloc(n, ev);
-  std::memcpy(ring.host + off, segs.data(), n);
   cudaStream_t st = dir == CS_D2H ? e->s_d2h : e->s_h2d;
   // a gather reads KV the last forward wrote; either direction may have to
   // follow a job of the other one that touches the same block / host slot
@@ -402,10 +405,83 @@ int64_t DeviceMover::launch(int dir, const std::vector<csb::Segment>& segs, int6
   if (after_other > 0) {
     if (cudaEvent_t w = pending_event(1 - dir, after_other)) CK(cudaStreamWaitEvent(st, w, 0));
   }
+  const int runs = e->L * 2 * e->hkv;
+  const size_t tok_elems = static_cast<size_t>(runs) * e->D;  // one token of one page, all layers
+  DescRing& ring = e->ring[dir];
   CK(cudaEventRecord(ev->start, st));
-  csk::kv_move(dir == CS_D2H, e->kv, e->host_kv_dev, ring.dev + off, static_cast<int>(segs.size()),
-               e->L * 2 * e->hkv, e->D, e->sms, st);
-  e->launches += 1;
+  if (e->kv_zerocopy) {
+    const size_t n = segs.size() * sizeof(csb::Segment);
+    const size_t off = ring.alloc(n, ev);
+    std::memcpy(ring.host + off, segs.data(), n);
+    csk::kv_move(dir == CS_D2H, e->kv, e->host_kv_dev, ring.dev + off, static_cast<int>(segs.size()), runs, e->D,
+                 e->sms, st);
+    e->launches += 1;
+  } else {
+    // chunks whose staging fits the buffer: pack (D2H) -> one batched DMA of
+    // the merged host runs -> (H2D) unpack; in stream order on this stream
+    const size_t seg_bytes = sizeof(csb::Segment) + sizeof(int64_t);
+    std::vector<void*> dsts, srcs;
+    std::vector<size_t> sizes;
+    size_t i0 = 0;
+    while (i0 < segs.size()) {
+      size_t i1 = i0, used = 0;
+      while (i1 < segs.size()) {
+        const size_t need = static_cast<size_t>(segs[i1].t1 - segs[i1].t0) * tok_elems;
+        if (i1 > i0 && used + need > e->stage_elems) break;
+        used += need;
+        ++i1;
+      }
+      const size_t n = i1 - i0;
+      const size_t off = ring.alloc(n * seg_bytes, ev);
+      std::memcpy(ring.host + off, segs.data() + i0, n * sizeof(csb::Segment));
+      int64_t* so = reinterpret_cast<int64_t*>(ring.host + off + n * sizeof(csb::Segment));
+      dsts.clear();
+      srcs.clear();
+      sizes.clear();
+      size_t pos = 0;
+      for (size_t k = i0; k < i1; ++k) {
+        const csb::Segment& g = segs[k];
+        so[k - i0] = static_cast<int64_t>(pos);
+        const size_t len = static_cast<size_t>(g.t1 - g.t0) * tok_elems * 2;
+        uint8_t* hp = reinterpret_cast<uint8_t*>(e->host_kv) +
+                      (static_cast<size_t>(g.slot) * 16 + static_cast<size_t>(g.t0)) * tok_elems * 2;
+        uint8_t* sp = reinterpret_cast<uint8_t*>(e->stage[dir] + pos);
+        void* d = dir == CS_D2H ? static_cast<void*>(hp) : static_cast<void*>(sp);
+        void* src = dir == CS_D2H ? static_cast<void*>(sp) : static_cast<void*>(hp);
+        // merge with the previous run when both sides continue it
+        if (!sizes.empty() && static_cast<uint8_t*>(dsts.back()) + sizes.back() == d &&
+            static_cast<uint8_t*>(srcs.back()) + sizes.back() == src) {
+          sizes.back() += len;
+        } else {
+          dsts.push_back(d);
+          srcs.push_back(src);
+          sizes.push_back(len);
+        }
+        pos += static_cast<size_t>(g.t1 - g.t0) * tok_elems;
+      }
+      const void* dseg = ring.dev + off;
+      const int64_t* dso = reinterpret_cast<const int64_t*>(ring.dev + off + n * sizeof(csb::Segment));
+      if (dir == CS_D2H) {
+        csk::kv_pack(true, e->kv, e->stage[dir], dseg, dso, static_cast<int>(n), runs, e->D, e->sms, st);
+        e->launches += 1;
+      }
+      cudaMemcpyAttributes attr{};
+      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+      size_t attr_idx = 0, fail = 0;
+      if (sizes.size() == 1) {
+        CK(cudaMemcpyAsync(dsts[0], srcs[0], sizes[0], cudaMemcpyDefault, st));
+      } else {
+        CK(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr, &attr_idx, 1, &fail,
+                                st));
+      }
+      if (dir == CS_H2D) {
+        csk::kv_pack(false, e->kv, e->stage[dir], dseg, dso, static_cast<int>(n), runs, e->D, e->sms, st);
+        e->launches += 1;
+      }
+      i0 = i1;
+    }
+  }
   CK(cudaGetLastError());
   CK(cudaEventRecord(ev->end, st));
   live[dir].push_back({++issued[dir], std::move(ev)});
@@ -1228,6 +1304,16 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
       CK(cudaHostAlloc(&e->host_kv, static_cast<size_t>(pc.n_slots) * blk_bytes,
                        cudaHostAllocMapped | cudaHostAllocPortable));
       CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->host_kv_dev), e->host_kv, 0));
+      {
+        const char* zc = std::getenv("CS_KV_ZEROCOPY");
+        e->kv_zerocopy = zc && zc[0] == '1';
+        if (!e->kv_zerocopy) {
+          // 256 MiB per direction (>= one page): a larger job runs as a
+          // sequence of pack + DMA chunks on its stream
+          e->stage_elems = std::max<size_t>(static_cast<size_t>(e->block_elems), (256u << 20) / 2);
+          for (int d = 0; d < 2; ++d) CK(cudaMalloc(&e->stage[d], e->stage_elems * 2));
+        }
+      }
       for (int d = 0; d < 2; ++d) {
         e->ring[d].cap = 8u << 20;
         CK(cudaHostAlloc(&e->ring[d].host, e->ring[d].cap, cudaHostAllocMapped | cudaHostAllocPortable));
@@ -1398,6 +1484,8 @@ int cs_destroy(cs_engine* e) {
       if (e->xchg) cudaFree(e->xchg);
       cudaFree(e->kv);
       cudaFreeHost(e->host_kv);
+      for (int d = 0; d < 2; ++d)
+        if (e->stage[d]) cudaFree(e->stage[d]);
       for (auto& r : e->ring) cudaFreeHost(r.host);
       cudaFreeHost(e->mailbox);
       cudaFree(e->weight_mem);
@@ -1981,7 +2069,13 @@ int cs_debug_read_host_slot(cs_engine* e, int32_t slot, void* dst, size_t bytes)
   return guard([&] {
     const size_t bb = static_cast<size_t>(e->block_elems) * 2;
     if (bytes < bb) throw std::invalid_argument("buffer too small");
-    std::memcpy(dst, e->host_kv + static_cast<size_t>(slot) * e->block_elems, bb);
+    // the slot is token-major [16][runs][D]; hand it out in the device
+    // block's run-major [runs][16][D] order so callers compare them directly
+    const size_t runs = static_cast<size_t>(e->L) * 2 * e->hkv, D = static_cast<size_t>(e->D);
+    const __nv_bfloat16* src = e->host_kv + static_cast<size_t>(slot) * e->block_elems;
+    auto* out = static_cast<__nv_bfloat16*>(dst);
+    for (size_t t = 0; t < 16; ++t)
+      for (size_t r = 0; r < runs; ++r) std::memcpy(out + (r * 16 + t) * D, src + (t * runs + r) * D, D * 2);
   });
 }
 int cs_debug_fill_pool(cs_engine* e, uint64_t seed) {

@@ -374,6 +374,14 @@ struct SegDesc {
   int32_t block, slot, t0, t1;
 };
 
+// Host slot layout (pinned pool): TOKEN-major, [16 tokens][runs][D] with
+// runs = L * 2 * H_kv(rank) -- a page's token range [t0, t1) is ONE
+// contiguous run of (t1 - t0) * runs * D elements, so a delta of a page is a
+// single copy-engine transfer. Device blocks stay run-major
+// [runs][16 tokens][D] (16 consecutive rows per (layer, K|V, head) for TMA).
+
+// Zero-copy variant (CS_KV_ZEROCOPY=1, A/B only): SM warps move 16-B vectors
+// straight between the block and the mapped pinned slot.
 template <bool kToHost>
 __global__ void __launch_bounds__(256) kv_move_kernel(__nv_bfloat16* pool, __nv_bfloat16* host,
                                                       const SegDesc* segs, int n_segs, int runs_per_seg, int D) {
@@ -381,20 +389,22 @@ __global__ void __launch_bounds__(256) kv_move_kernel(__nv_bfloat16* pool, __nv_
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const size_t block_elems = static_cast<size_t>(runs_per_seg) * 16 * D;
-  const int vec_per_tok = D / 8;
+  const int vpt = D / 8;  // 16-B vectors per token row
   for (int64_t item = w; item < static_cast<int64_t>(n_segs) * runs_per_seg; item += warps) {
     const int s = static_cast<int>(item / runs_per_seg);
     const int run = static_cast<int>(item % runs_per_seg);
     const SegDesc sd = segs[s];
-    const size_t off = static_cast<size_t>(run) * 16 * D + static_cast<size_t>(sd.t0) * D;
-    uint4* dev = reinterpret_cast<uint4*>(pool + static_cast<size_t>(sd.block) * block_elems + off);
-    uint4* hst = reinterpret_cast<uint4*>(host + static_cast<size_t>(sd.slot) * block_elems + off);
-    const int n = (sd.t1 - sd.t0) * vec_per_tok;
+    uint4* dev = reinterpret_cast<uint4*>(pool + static_cast<size_t>(sd.block) * block_elems +
+                                          static_cast<size_t>(run) * 16 * D + static_cast<size_t>(sd.t0) * D);
+    uint4* hst = reinterpret_cast<uint4*>(host + static_cast<size_t>(sd.slot) * block_elems +
+                                          (static_cast<size_t>(sd.t0) * runs_per_seg + run) * D);
+    const int n = (sd.t1 - sd.t0) * vpt;
     for (int i = lane; i < n; i += 32) {
+      const size_t h = static_cast<size_t>(i / vpt) * runs_per_seg * vpt + (i % vpt);
       if (kToHost) {
-        hst[i] = __ldcs(dev + i);
+        hst[h] = __ldcs(dev + i);
       } else {
-        dev[i] = hst[i];
+        dev[i] = hst[h];
       }
     }
   }
@@ -404,21 +414,68 @@ void kv_move(bool to_host, __nv_bfloat16* pool, __nv_bfloat16* host_mapped, cons
              int runs_per_seg, int D, int sms, cudaStream_t s) {
   if (n_segs <= 0) return;
   const int64_t items = static_cast<int64_t>(n_segs) * runs_per_seg;
-  // The copy is host-link bound (~57 GB/s): a few CTAs per SM keep enough
-  // stores in flight, more only take thread slots from the concurrent forward.
-  static const int per_sm = [] {
-    const char* v = std::getenv("CS_KV_MOVE_CTAS_PER_SM");
-    const int n = v ? std::atoi(v) : 2;  // profiles/r1/SUMMARY.md (calls r2p, r2q)
-    return n < 1 ? 1 : n;
-  }();
+  // host-link bound (~57 GB/s): a few CTAs per SM keep enough stores in
+  // flight, more only take thread slots from the concurrent forward
   int64_t grid = (items + 7) / 8;
-  if (grid > static_cast<int64_t>(sms) * per_sm) grid = static_cast<int64_t>(sms) * per_sm;
+  if (grid > static_cast<int64_t>(sms) * 2) grid = static_cast<int64_t>(sms) * 2;
   if (grid < 1) grid = 1;
   const SegDesc* sd = static_cast<const SegDesc*>(segs_mapped);
   if (to_host) {
     kv_move_kernel<true><<<static_cast<int>(grid), 256, 0, s>>>(pool, host_mapped, sd, n_segs, runs_per_seg, D);
   } else {
     kv_move_kernel<false><<<static_cast<int>(grid), 256, 0, s>>>(pool, host_mapped, sd, n_segs, runs_per_seg, D);
+  }
+}
+
+// K4 / K5 (default): HBM <-> HBM pack / unpack between the blocks and a
+// device staging buffer laid out like the host slots (token-major), so the
+// host-link leg is plain copy-engine DMA (cudaMemcpyBatchAsync) and no SM
+// sits on PCIe latency for the length of the transfer. Segment s occupies
+// staging elements [stage[s], stage[s] + (t1 - t0) * runs * D).
+// One warp per (segment, run): 16-B vectors, the block side contiguous, the
+// staging side in 2*D-byte rows.
+template <bool kToStage>
+__global__ void __launch_bounds__(256) kv_pack_kernel(__nv_bfloat16* pool, __nv_bfloat16* stage,
+                                                      const SegDesc* segs, const int64_t* stage_off, int n_segs,
+                                                      int runs_per_seg, int D) {
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const size_t block_elems = static_cast<size_t>(runs_per_seg) * 16 * D;
+  const int vpt = D / 8;
+  for (int64_t item = w; item < static_cast<int64_t>(n_segs) * runs_per_seg; item += warps) {
+    const int s = static_cast<int>(item / runs_per_seg);
+    const int run = static_cast<int>(item % runs_per_seg);
+    const SegDesc sd = segs[s];
+    uint4* dev = reinterpret_cast<uint4*>(pool + static_cast<size_t>(sd.block) * block_elems +
+                                          static_cast<size_t>(run) * 16 * D + static_cast<size_t>(sd.t0) * D);
+    uint4* stg = reinterpret_cast<uint4*>(stage + stage_off[s] + static_cast<size_t>(run) * D);
+    const int n = (sd.t1 - sd.t0) * vpt;
+    for (int i = lane; i < n; i += 32) {
+      const size_t h = static_cast<size_t>(i / vpt) * runs_per_seg * vpt + (i % vpt);
+      if (kToStage) {
+        stg[h] = __ldcs(dev + i);
+      } else {
+        dev[i] = __ldcs(stg + h);
+      }
+    }
+  }
+}
+
+void kv_pack(bool to_stage, __nv_bfloat16* pool, __nv_bfloat16* stage, const void* segs, const int64_t* stage_off,
+             int n_segs, int runs_per_seg, int D, int sms, cudaStream_t s) {
+  if (n_segs <= 0) return;
+  const int64_t items = static_cast<int64_t>(n_segs) * runs_per_seg;
+  // HBM-bound and short (2 x bytes at ~6.5 TB/s): 8 warps per CTA, up to 4
+  // CTAs per SM, each warp a (segment, run) of <= 16 rows
+  int64_t grid = (items + 7) / 8;
+  if (grid > static_cast<int64_t>(sms) * 4) grid = static_cast<int64_t>(sms) * 4;
+  if (grid < 1) grid = 1;
+  const SegDesc* sd = static_cast<const SegDesc*>(segs);
+  if (to_stage) {
+    kv_pack_kernel<true><<<static_cast<int>(grid), 256, 0, s>>>(pool, stage, sd, stage_off, n_segs, runs_per_seg, D);
+  } else {
+    kv_pack_kernel<false><<<static_cast<int>(grid), 256, 0, s>>>(pool, stage, sd, stage_off, n_segs, runs_per_seg, D);
   }
 }
 
