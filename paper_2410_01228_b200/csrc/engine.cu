@@ -275,9 +275,9 @@ struct cs_engine {
   bool lt_gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
   // K7 (csrc/gemm_tc.cu): the M <= 256 projections on our own tcgen05
   // weight-streaming kernel; TMA maps per (tensor, rows, K, box rows)
-  // 0 never (default: cuBLAS wins the decode step, profiles/r1/k7_gemm.md), 1 always for M <= 256
-  // (CS_WGEMM=1), 2 where tune_gemms timed it faster than the best cuBLAS plan (CS_WGEMM=2)
-  int wgemm_mode = 0;
+  // 0 never (CS_WGEMM=0), 1 always for M <= 256 (CS_WGEMM=1), 2 (default) where tune_gemms
+  // timed it faster than the best cuBLAS plan
+  int wgemm_mode = 2;
   std::map<uint64_t, bool> k7_pick;
   std::map<std::pair<int, int>, int> k7_clusters;  // (Mp, K split) -> co-resident clusters (per engine: no shared state)
   std::map<std::tuple<const void*, int, int, int>, CUtensorMap> tmaps;
@@ -717,16 +717,19 @@ bool cs_engine::wgemm_launch(const __nv_bfloat16* A, const __nv_bfloat16* W, voi
   const CUtensorMap* wm = tmap(W, N, K, 128);
   const CUtensorMap* xm = tmap(A, M, K, Mp);
   if (!wm || !xm) return false;
-  // one wave: >= one feature tile per SM -> two CTAs per SM, no split;
-  // fewer tiles -> one deep-ring CTA per SM and a K split (a cluster of <= 8)
+  // ONE wave of CTAs: >= one feature tile per SM -> two CTAs per SM, no
+  // split; fewer tiles -> one deep-ring CTA per SM and the largest K split
+  // (a cluster of <= 8, any size, uneven last split) with n_tiles x split <=
+  // SMs whose clusters are all co-resident. A second wave would double the
+  // prologue + epilogue the weight stream cannot hide (qkv at split 4: 192
+  // CTAs on 148 SMs ran at 2 TB/s, profiles/r1/k7_gemm.md).
   const int n_tiles = N / 128;
   const bool two = n_tiles >= sms;
   const int stages = csk::wgemm_stages(Mp, two ? 112 * 1024 : 220 * 1024);
   int splits = 1;
   if (!two) {
-    // the largest power-of-two K split whose clusters all fit at once
-    for (int sp = 8; sp >= 2; sp /= 2) {
-      if (n_tiles * sp > 2 * sms || K / 64 / sp < 4) continue;
+    for (int sp = 8; sp >= 2; --sp) {
+      if (n_tiles * sp > sms || K / 64 / sp < 4) continue;
       auto key = std::make_pair(Mp, sp);
       auto f = k7_clusters.find(key);
       if (f == k7_clusters.end()) f = k7_clusters.emplace(key, csk::wgemm_max_clusters(Mp, stages, sp)).first;
@@ -1403,8 +1406,10 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         CKB(cublasSetMathMode(e->blas, CUBLAS_DEFAULT_MATH));
         CKB(cublasLtCreate(&e->lt));
         {
-          const char* v = std::getenv("CS_WGEMM");  // K7 for the M <= 256 projections
-          e->wgemm_mode = (v && v[0] == '1') ? 1 : (v && v[0] == '2') ? 2 : 0;
+          // K7 for the M <= 256 projections: 2 (default) where start-up
+          // tuning timed it faster than the best cuBLAS plan, 1 always, 0 never
+          const char* v = std::getenv("CS_WGEMM");
+          e->wgemm_mode = (v && v[0] == '1') ? 1 : (v && v[0] == '0') ? 0 : 2;
         }
         // Workspaces and the metadata buffer at their upper bounds, so no
         // iteration frees device memory (cudaFree synchronises the device:
