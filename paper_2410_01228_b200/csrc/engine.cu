@@ -44,7 +44,7 @@ void add_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16
                  float eps, const IterDesc* desc, const int32_t* row_idx, int grid, cudaStream_t s,
                  const SafepointArg& sp = SafepointArg{});
 void silu_mul(const __nv_bfloat16* gu, __nv_bfloat16* act, int ffn, const IterDesc* desc, int grid_rows,
-              cudaStream_t s);
+              cudaStream_t s, bool interleave);
 void rope_append(__nv_bfloat16* qkv, const int32_t* tok_pos, const int32_t* tok_slot, __nv_bfloat16* pool, int hq,
                  int hkv, int D, int num_layers, int layer, float theta, const IterDesc* desc, int grid,
                  cudaStream_t s);
@@ -70,7 +70,7 @@ void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, 
 void p2p_allreduce(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s);
 bool gemm_pf_supported(int N, int K);
 void gemm_pf(const CUtensorMap* xmap, const CUtensorMap* wmap, void* y, int M, const int32_t* m_dev, int N, int K,
-             bool f32_out, int sms, cudaStream_t s);
+             bool f32_out, int sms, cudaStream_t s, bool swiglu = false);
 }  // namespace csk
 
 namespace {
@@ -370,6 +370,10 @@ struct cs_engine {
   bool use_pf(int M, int N, int K) const;
   int pf_min_rows = 2048;
   bool pf_enabled = true;
+  // W_gate|up stored interleaved in 128-row blocks ([g 0..127 | u 0..127 |
+  // g 128..255 | ...]) so a 256-column K8 tile holds matching gate and up
+  // features and its epilogue writes silu(g) * u directly (ffn % 128 == 0)
+  bool gu_interleave = false;
   void allreduce(__nv_bfloat16* buf, int64_t count);
   // ---- peer-memory all-reduce: exchange region =
   // [2 partial buffers of (max_tok*hidden + 64) bf16][flag u64][step u64][arrive i32]
@@ -850,8 +854,22 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
       reduce_into(tmp, M * hidden);
     }
     csk::add_rmsnorm(x, tmp, w.mlp_norm[l], xn, hidden, cfg.rms_eps, desc, nullptr, T, s_compute);
-    n_launch += gemm(xn, w.wgu[l], gu, static_cast<int>(M), 2 * ffn, hidden, false, m_dev);
-    csk::silu_mul(gu, act, ffn, desc, T, s_compute);
+    const CUtensorMap* gxm = nullptr;
+    const CUtensorMap* gwm = nullptr;
+    if (gu_interleave && use_pf(static_cast<int>(M), 2 * ffn, hidden)) {
+      gxm = tmap(xn, static_cast<int>(max_tok), hidden, 128);
+      gwm = tmap(w.wgu[l], 2 * ffn, hidden, 128);
+    }
+    if (gxm && gwm) {  // K8 with the SwiGLU epilogue: gate|up never round-trips through HBM
+      timed(CS_KT_K8, 2.0 * M * 2 * ffn * hidden, [&] {
+        csk::gemm_pf(gxm, gwm, act, static_cast<int>(M), m_dev, 2 * ffn, hidden, false, sms, s_compute, true);
+      });
+      n_launch += 1;
+    } else {
+      n_launch += gemm(xn, w.wgu[l], gu, static_cast<int>(M), 2 * ffn, hidden, false, m_dev);
+      csk::silu_mul(gu, act, ffn, desc, T, s_compute, gu_interleave);
+      n_launch += 1;
+    }
     {
       __nv_bfloat16* part = partial_out(tmp);
       n_launch += gemm(act, w.wd[l], part, static_cast<int>(M), hidden, ffn, false, m_dev);
@@ -867,7 +885,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
         }
       }
     }
-    n_launch += (l == 0 ? 1 : 0) + 4 + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
+    n_launch += (l == 0 ? 1 : 0) + 3 + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
                 (it.n_dec > 0 ? 1 : 0) + (it.n_pt > 0 ? (it.k2_splits > 1 ? 2 : 1) : 0);
     if ((cfg.flags & CS_FLAG_SYNC_DEBUG) && !graph) {
       CK(cudaStreamSynchronize(s_compute));
@@ -1351,6 +1369,12 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         csk::init_matrix(e->w.lm_head, e->vocab, H, H, 0, ident, seed, kTensorLm, wscale, 0.f, s);
         csk::init_matrix(e->w.final_norm, 1, H, H, 0, ident, seed, kTensorFinalNorm, 0.1f, 1.f, s);
         const int64_t Hq_g = cfg->n_heads, Hkv_g = cfg->n_kv_heads, F_g = cfg->ffn;
+        {
+          const char* v = std::getenv("CS_NO_GU_INTERLEAVE");
+          e->gu_interleave = e->ffn % 128 == 0 && !(v && v[0] == '1');
+        }
+        __nv_bfloat16* gu_tmp = nullptr;
+        if (e->gu_interleave) CK(cudaMalloc(&gu_tmp, 2LL * e->ffn * H * 2));
         for (int l = 0; l < e->L; ++l) {
           e->w.attn_norm.push_back(take(H));
           e->w.wqkv.push_back(take(qkv_rows * H));
@@ -1372,11 +1396,25 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
                            ident, seed, tensor_id(l, kWO), wscale, 0.f, s);
           csk::RowMap gu_map{2, {0, e->ffn, 0}, {static_cast<int64_t>(e->rank) * e->ffn,
                                                  F_g + static_cast<int64_t>(e->rank) * e->ffn, 0}};
-          csk::init_matrix(e->w.wgu[l], 2LL * e->ffn, H, H, 0, gu_map, seed, tensor_id(l, kWGu), wscale, 0.f, s);
+          if (e->gu_interleave) {
+            // init in the gate | up order, then 128-row blocks interleaved
+            const size_t blk = static_cast<size_t>(128) * H * 2;
+            csk::init_matrix(gu_tmp, 2LL * e->ffn, H, H, 0, gu_map, seed, tensor_id(l, kWGu), wscale, 0.f, s);
+            CK(cudaMemcpy2DAsync(e->w.wgu[l], 2 * blk, gu_tmp, blk, blk, e->ffn / 128, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpy2DAsync(reinterpret_cast<uint8_t*>(e->w.wgu[l]) + blk, 2 * blk,
+                                 gu_tmp + static_cast<size_t>(e->ffn) * H, blk, blk, e->ffn / 128,
+                                 cudaMemcpyDeviceToDevice, s));
+          } else {
+            csk::init_matrix(e->w.wgu[l], 2LL * e->ffn, H, H, 0, gu_map, seed, tensor_id(l, kWGu), wscale, 0.f, s);
+          }
           csk::init_matrix(e->w.wd[l], H, e->ffn, F_g, static_cast<int64_t>(e->rank) * e->ffn, ident, seed,
                            tensor_id(l, kWD), wscale, 0.f, s);
         }
         CK(cudaGetLastError());
+        if (gu_tmp) {
+          CK(cudaStreamSynchronize(s));
+          CK(cudaFree(gu_tmp));
+        }
         // activations
         const int64_t T = e->max_tok;
         CK(cudaMalloc(&e->x, T * H * 2));
@@ -2107,7 +2145,17 @@ int cs_debug_read_weight(cs_engine* e, int32_t layer, int32_t which, void* dst, 
       default: throw std::invalid_argument("unknown weight");
     }
     *needed = static_cast<size_t>(n) * 2;
-    if (dst && bytes >= *needed) CK(cudaMemcpy(dst, src, *needed, cudaMemcpyDeviceToHost));
+    if (dst && bytes >= *needed) {
+      if (which == 4 && e->gu_interleave) {  // hand out the gate | up order
+        const size_t blk = static_cast<size_t>(128) * H * 2;
+        CK(cudaMemcpy2D(dst, blk, src, 2 * blk, blk, e->ffn / 128, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy2D(static_cast<uint8_t*>(dst) + static_cast<size_t>(e->ffn) * H * 2, blk,
+                        reinterpret_cast<const uint8_t*>(src) + blk, 2 * blk, blk, e->ffn / 128,
+                        cudaMemcpyDeviceToHost));
+      } else {
+        CK(cudaMemcpy(dst, src, *needed, cudaMemcpyDeviceToHost));
+      }
+    }
   });
 }
 int cs_debug_read_activation(cs_engine* e, int32_t which, void* dst, size_t bytes) {

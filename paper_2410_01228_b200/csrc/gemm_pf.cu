@@ -49,6 +49,7 @@ struct PfArgs {
   int32_t M, N, K;       // M: host upper bound (rows of the X tensor map)
   int32_t f32_out;
   int32_t band;          // m-tiles per raster band (L2 reuse of the X and W panels)
+  int32_t swiglu;        // W = gate|up interleaved in 128-row blocks: y = silu(gate) * up [M, N / 2]
 };
 
 // Tile t -> (m tile, n tile): bands of `band` m-tiles, m fastest inside a
@@ -173,6 +174,40 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       const int row = tm * 2 * kPfRows + static_cast<int>(rank) * kPfRows + q * 32 + lane;
       const int n0 = tn * kPfN;
       const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * kPfN;
+      if (a.swiglu) {
+        // fused SwiGLU: TMEM columns [0, 128) = gate, [128, 256) = up of the
+        // same 128 FFN features; rounded to bf16 first, as the unfused path
+        // stores gate|up, then silu(g) * u -> act[row, tn * 128 + c]
+#pragma unroll 1
+        for (int c = 0; c < kPfN / 2; c += 32) {
+          float g[32], u[32];
+          tc::tmem_ld32(tl + c, g);
+          tc::tmem_ld32(tl + kPfN / 2 + c, u);
+          tc::tmem_wait_ld();
+          tc::reg_fence<32>(g);
+          tc::reg_fence<32>(u);
+          if (row < M) {
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.y) +
+                                                  static_cast<size_t>(row) * (a.N / 2) + tn * (kPfN / 2) + c);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float o[8];
+#pragma unroll
+              for (int t = 0; t < 8; ++t) {
+                const float gf = __bfloat162float(__float2bfloat16(g[8 * j + t]));
+                const float uf = __bfloat162float(__float2bfloat16(u[8 * j + t]));
+                o[t] = gf / (1.f + __expf(-gf)) * uf;
+              }
+              dst[j] = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]),
+                                  pack_bf16(o[6], o[7]));
+            }
+          }
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_cluster(tempty0 + acc * 8);
+        continue;
+      }
 #pragma unroll 1
       for (int c = 0; c < kPfN; c += 32) {
         float v[32];
@@ -214,7 +249,7 @@ int gemm_pf_rows_box() { return kPfRows; }
 // [N][K], both 64 x 128 boxes with 128-B swizzle. M is the host bound (grid
 // size); m_dev, when set, the live row count read by the kernel.
 void gemm_pf(const CUtensorMap* xmap, const CUtensorMap* wmap, void* y, int M, const int32_t* m_dev, int N, int K,
-             bool f32_out, int sms, cudaStream_t s) {
+             bool f32_out, int sms, cudaStream_t s, bool swiglu) {
   smem_attr_once(reinterpret_cast<const void*>(gemm_pf_kernel), kPfSmem);
   PfArgs a{};
   a.y = y;
@@ -223,6 +258,7 @@ void gemm_pf(const CUtensorMap* xmap, const CUtensorMap* wmap, void* y, int M, c
   a.N = N;
   a.K = K;
   a.f32_out = f32_out ? 1 : 0;
+  a.swiglu = swiglu ? 1 : 0;
   static const int band_env = [] {
     const char* v = std::getenv("CS_PF_BAND");
     return v ? std::atoi(v) : 0;

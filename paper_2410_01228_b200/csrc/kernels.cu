@@ -184,16 +184,21 @@ void add_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16
 }
 
 // ----------------------------------------------------------------- SwiGLU ----
-__global__ void silu_mul_kernel(const __nv_bfloat16* gu, __nv_bfloat16* act, int ffn, const IterDesc* desc) {
+// act[t, c] = silu(gate[t, c]) * up[t, c]. gu row layout: gate | up
+// (interleave = 0) or gate|up interleaved in 128-column blocks (the weight
+// layout K8 fuses this into its epilogue with; interleave = 1).
+__global__ void silu_mul_kernel(const __nv_bfloat16* gu, __nv_bfloat16* act, int ffn, const IterDesc* desc,
+                                int interleave) {
   pdl_trigger();
   const int t = blockIdx.y;
   if (t >= desc->n_tok_cur) return;
-  const __nv_bfloat16* g = gu + static_cast<size_t>(t) * 2 * ffn;
-  const __nv_bfloat16* u = g + ffn;
+  const __nv_bfloat16* row = gu + static_cast<size_t>(t) * 2 * ffn;
   __nv_bfloat16* a = act + static_cast<size_t>(t) * ffn;
   for (int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8; c < ffn; c += gridDim.x * blockDim.x * 8) {
-    uint4 gv = *reinterpret_cast<const uint4*>(g + c);
-    uint4 uv = *reinterpret_cast<const uint4*>(u + c);
+    const int gc = interleave ? (c >> 7) * 256 + (c & 127) : c;
+    const int uc = interleave ? gc + 128 : c + ffn;
+    uint4 gv = *reinterpret_cast<const uint4*>(row + gc);
+    uint4 uv = *reinterpret_cast<const uint4*>(row + uc);
     const __nv_bfloat16* ge = reinterpret_cast<const __nv_bfloat16*>(&gv);
     const __nv_bfloat16* ue = reinterpret_cast<const __nv_bfloat16*>(&uv);
     __nv_bfloat16 o[8];
@@ -207,10 +212,11 @@ __global__ void silu_mul_kernel(const __nv_bfloat16* gu, __nv_bfloat16* act, int
 }
 
 void silu_mul(const __nv_bfloat16* gu, __nv_bfloat16* act, int ffn, const IterDesc* desc, int grid_rows,
-              cudaStream_t s) {
+              cudaStream_t s, bool interleave) {
   if (grid_rows <= 0) return;
   const int bx = (ffn / 8 + 255) / 256;
-  silu_mul_kernel<<<dim3(bx < 1 ? 1 : (bx > 16 ? 16 : bx), grid_rows), 256, 0, s>>>(gu, act, ffn, desc);
+  silu_mul_kernel<<<dim3(bx < 1 ? 1 : (bx > 16 ? 16 : bx), grid_rows), 256, 0, s>>>(gu, act, ffn, desc,
+                                                                                  interleave ? 1 : 0);
 }
 
 // ------------------------------------------------- RoPE + KV append (K3) ----

@@ -17,7 +17,7 @@
 
 namespace csk {
 void gemm_pf(const CUtensorMap* xmap, const CUtensorMap* wmap, void* y, int M, const int32_t* m_dev, int N, int K,
-             bool f32_out, int sms, cudaStream_t s);
+             bool f32_out, int sms, cudaStream_t s, bool swiglu);
 }
 
 #define CK(x)                                                                       \
@@ -99,7 +99,7 @@ int main(int argc, char** argv) {
       // device M smaller than the host bound for one case: tiles past it must not be written
       CK(cudaMemsetAsync(y1, 0, static_cast<size_t>(M) * sh.N * 2, s));
       CK(cudaMemcpyAsync(d_m, &M, 4, cudaMemcpyHostToDevice, s));
-      csk::gemm_pf(&xm, &wm[0], y1, Mmax, d_m, sh.N, sh.K, false, sms, s);
+      csk::gemm_pf(&xm, &wm[0], y1, Mmax, d_m, sh.N, sh.K, false, sms, s, false);
       const float alpha = 1.f, beta = 0.f;
       cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, sh.N, M, sh.K, &alpha, w, CUDA_R_16BF, sh.K, x, CUDA_R_16BF, sh.K,
                    &beta, y2, CUDA_R_16BF, sh.N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
@@ -119,7 +119,7 @@ int main(int argc, char** argv) {
         for (int r = 0; r < 3 + reps; ++r) {
           if (r == 3) CK(cudaEventRecord(e0, s));
           if (k8) {
-            csk::gemm_pf(&xm, &wm[r % copies], y1, M, nullptr, sh.N, sh.K, false, sms, s);
+            csk::gemm_pf(&xm, &wm[r % copies], y1, M, nullptr, sh.N, sh.K, false, sms, s, false);
           } else {
             cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, sh.N, M, sh.K, &alpha, w + nw * (r % copies), CUDA_R_16BF,
                          sh.K, x, CUDA_R_16BF, sh.K, &beta, y2, CUDA_R_16BF, sh.N, CUBLAS_COMPUTE_32F,

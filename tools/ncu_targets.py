@@ -3,6 +3,7 @@
   python tools/ncu_targets.py decode    # K1: 64 seqs x 4224 ctx, Llama-3.1-8B heads
   python tools/ncu_targets.py prefill   # K2: one 2048-token chunk over 4096 cached
   python tools/ncu_targets.py gather    # K4: checkpoint gather of 1024 whole blocks
+  python tools/ncu_targets.py gemm      # K8: 8192-token prefill forwards of the full 8B
 
 Each target launches its kernel a handful of times (ncu replays each launch);
 the numbers printed here are NOT bench values.
@@ -90,6 +91,22 @@ def step(n=32, ctx=4096, reps=3):
     eng.close()
 
 
+def gemm(P=8192, reps=2):
+    """Prefill forwards of the full Llama-3.1-8B over one P-token chunk: the
+    layer projections run on K8 (gemm_pf_kernel, gate|up with the fused
+    SwiGLU epilogue)."""
+    cfg = cs.model_config("llama8b", gpu_kv_capacity=8 << 30, host_kv_capacity=1 << 30, max_batched_tokens=8192,
+                          instrumented=0, max_entries=256)
+    eng = cs.Engine(cfg)
+    for rep in range(reps):
+        eng.register_request(rep, False)
+        assert eng.allocate(rep, P).ok
+        info = eng.forward([cs.BatchEntry(rep, P, 0, cs.CS_PREFILL, False)], epoch=rep + 1)
+        eng.commit_allocations(rep)
+        print(f"prefill forward {P} tokens: {info.gpu_ms:.3f} ms", flush=True)
+    eng.close()
+
+
 if __name__ == "__main__":
     # optional integer arguments are passed through, e.g. `step 92 4130`
-    {"decode": decode, "prefill": prefill, "gather": gather, "step": step}[sys.argv[1]](*map(int, sys.argv[2:]))
+    {"decode": decode, "prefill": prefill, "gather": gather, "step": step, "gemm": gemm}[sys.argv[1]](*map(int, sys.argv[2:]))
