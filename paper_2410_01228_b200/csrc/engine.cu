@@ -421,7 +421,7 @@ int64_t DeviceMover::launch(int dir, const std::vector<csb::Segment>& segs, int6
                  e->sms, st);
     e->launches += 1;
   } else {
-    // chunks whose staging fits the buffer: pack (D2H) -> one batched DMA of
+    // chunks whose staging fits the buffer: pack (D2H) -> copy-engine DMA of
     // the merged host runs -> (H2D) unpack; in stream order on this stream
     const size_t seg_bytes = sizeof(csb::Segment) + sizeof(int64_t);
     std::vector<void*> dsts, srcs;
@@ -469,16 +469,9 @@ int64_t DeviceMover::launch(int dir, const std::vector<csb::Segment>& segs, int6
         csk::kv_pack(true, e->kv, e->stage[dir], dseg, dso, static_cast<int>(n), runs, e->D, e->sms, st);
         e->launches += 1;
       }
-      cudaMemcpyAttributes attr{};
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-      size_t attr_idx = 0, fail = 0;
-      if (sizes.size() == 1) {
-        CK(cudaMemcpyAsync(dsts[0], srcs[0], sizes[0], cudaMemcpyDefault, st));
-      } else {
-        CK(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr, &attr_idx, 1, &fail,
-                                st));
-      }
+      // one copy-engine DMA per merged host run (host slots are token-major,
+      // so adjacent slots of one job usually merge into a few long runs)
+      for (size_t k = 0; k < sizes.size(); ++k) CK(cudaMemcpyAsync(dsts[k], srcs[k], sizes[k], cudaMemcpyDefault, st));
       if (dir == CS_H2D) {
         csk::kv_pack(false, e->kv, e->stage[dir], dseg, dso, static_cast<int>(n), runs, e->D, e->sms, st);
         e->launches += 1;

@@ -435,7 +435,8 @@ void kv_move(bool to_host, __nv_bfloat16* pool, __nv_bfloat16* host_mapped, cons
 
 // K4 / K5 (default): HBM <-> HBM pack / unpack between the blocks and a
 // device staging buffer laid out like the host slots (token-major), so the
-// host-link leg is plain copy-engine DMA (cudaMemcpyBatchAsync) and no SM
+// host-link leg is plain copy-engine DMA (one cudaMemcpyAsync per merged
+// host run) and no SM
 // sits on PCIe latency for the length of the transfer. Segment s occupies
 // staging elements [stage[s], stage[s] + (t1 - t0) * runs * D).
 // One warp per (segment, run): 16-B vectors, the block side contiguous, the

@@ -3,10 +3,10 @@
 # run and one `--set full` capture per hot-path kernel. Everything lands in
 # gpurun_out/ (copy the summaries worth keeping into profiles/).
 #   gpurun --timeout 2400 -- 'bash tools/gpu_round.sh [tag] [parts]'
-#   parts: comma list of probe,tests,bench,launches,k1,k2,k4 (default all)
+#   parts: comma list of probe,smoke,tests,bench,launches,k1,k2,k4,k8 (default all)
 set -u
 TAG=${1:-r1}
-PARTS=${2:-probe,smoke,tests,bench,launches,k1,k2,k4}
+PARTS=${2:-probe,smoke,tests,bench,launches,k1,k2,k4,k8}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 has() { [[ ",$PARTS," == *",$1,"* ]]; }
@@ -28,6 +28,10 @@ fi
 if has k2; then
   timeout 600 $NCU --set full --import-source on -k regex:attn_prefill -s 1 -c 1 -o "$OUT/k2_prefill" -f \
     python tools/ncu_targets.py prefill > "$OUT/k2.log" 2>&1
+fi
+if has k8; then
+  timeout 600 $NCU --set full --import-source on -k regex:gemm_pf -s 4 -c 1 -o "$OUT/k8_gemm" -f \
+    python tools/ncu_targets.py gemm > "$OUT/k8.log" 2>&1
 fi
 if has k4; then
   timeout 600 $NCU --set full --import-source on -k regex:kv_move -c 1 -o "$OUT/k4_gather" -f \

@@ -88,21 +88,6 @@ int main() {
       cudaEventRecord(e1, st); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1); best = std::min(best, ms);
     }
     printf("per-page DMA H2D 256 x 2MiB: %.1f GB/s\n", npages * pb / (best * 1e-3) / 1e9);
-    for (int seg : {4096, 65536}) {
-      int n = (int)(hostsz / seg) / 4;
-      std::vector<void*> srcs(n), dsts(n); std::vector<size_t> sizes(n, seg);
-      for (int i = 0; i < n; ++i) { srcs[i] = (char*)d + (size_t)((i * 7919ll) % (pool / seg)) * seg; dsts[i] = (char*)h + (size_t)i * seg; }
-      cudaMemcpyAttributes attr{}; attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream; attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-      size_t attrIdx = 0, fail = 0;
-      best = 1e9;
-      for (int r = 0; r < 3; ++r) {
-        cudaEventRecord(e0, st);
-        cudaError_t err = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &attrIdx, 1, &fail, st);
-        if (err != cudaSuccess) { printf("batch err %s\n", cudaGetErrorString(err)); break; }
-        cudaEventRecord(e1, st); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1); best = std::min(best, ms);
-      }
-      printf("cudaMemcpyBatchAsync D2H %d x %d B: %.1f GB/s\n", n, seg, (double)n * seg / (best * 1e-3) / 1e9);
-    }
   }
   return 0;
 }
