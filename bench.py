@@ -399,17 +399,22 @@ def attention_probe(cs, F, hbm_peak, bf16_peak):
     return out
 
 
-def safepoint_overhead(cs, F, reps=8):
+def safepoint_overhead(cs, F, reps=8, shard=None, attach=None, reduce_max=None):
     """SPEC.md acceptance #6: the same unpreempted mixed plan (online decode +
     offline 2048-token chunk) with a safepoint every layer vs none,
-    alternating engines so clock drift hits both."""
+    alternating engines so clock drift hits both. Under the north-star split
+    (`shard` = tp_size/tp_rank, every rank calls this) the instrumented engine
+    also votes in every all-reduce tail, so `frac` is the g-rank agreement
+    cost (reference model: preemption.cpp:15-22), max over ranks."""
     engs = []
     try:
         for instrumented in (0, 1):
             c = cs.model_config("llama8b", gpu_kv_capacity=8 << 30, host_kv_capacity=1 << 30,
                                 max_batched_tokens=8192, safepoint_interval_layers=1, instrumented=instrumented,
-                                max_entries=256)
+                                max_entries=256, **(shard or {}))
             e = cs.Engine(c)
+            if attach:
+                attach(e)
             e.register_request(0, True)
             e.register_request(1, False)
             assert e.allocate(0, 2049).ok
@@ -425,8 +430,12 @@ def safepoint_overhead(cs, F, reps=8):
                 if t >= 2:
                     times[i].append(ms)
         a, b = float(np.median(times[0])), float(np.median(times[1]))
-        return {"ms_without": a, "ms_with": b, "frac": b / a - 1.0, "reps": reps,
-                "plan": "online decode (C=2049) + offline 2048-token prefill chunk, 32 layers, 31 safepoints"}
+        if reduce_max:
+            a, b = reduce_max(a), reduce_max(b)
+        g = (shard or {}).get("tp_size", 1)
+        return {"ms_without": a, "ms_with": b, "frac": b / a - 1.0, "reps": reps, "tp": g,
+                "plan": "online decode (C=2049) + offline 2048-token prefill chunk, 32 layers, 31 safepoints"
+                        + (f", vote in every all-reduce tail of {g} ranks (max over ranks)" if g > 1 else "")}
     except Exception as ex:  # never hide the main numbers
         return {"error": str(ex)}
     finally:
@@ -474,6 +483,20 @@ def live_leg(name, device, margin=None):
             "transferred_bytes": m["transferred_bytes"], "wall_s": summ["wall_s"]}
 
 
+def ckpt_ranks(rows):
+    """N>1: per-rank checkpoint / restore GB/s (each rank's shard over its own
+    host link) and the aggregate (all ranks' bytes over the slowest rank's
+    summed copy time)."""
+    if not rows:
+        return {}
+    gbs = lambda b, ms: b / (ms * 1e-3) / 1e9 if ms > 0 else None
+    per = [{"rank": i, "d2h_gbs": gbs(r[0], r[1]), "h2d_gbs": gbs(r[2], r[3]), "d2h_bytes": int(r[0]),
+            "h2d_bytes": int(r[2]), "host_numa_node": int(r[4])} for i, r in enumerate(rows)]
+    return {"per_rank": per,
+            "aggregate_d2h_gbs": gbs(sum(r[0] for r in rows), max(r[1] for r in rows)),
+            "aggregate_h2d_gbs": gbs(sum(r[2] for r in rows), max(r[3] for r in rows))}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -512,6 +535,22 @@ def main():
     tp = world > 1 and not args.replicas
     mode = mode_of(world, args.replicas)
 
+    def attach_tp(eng):
+        """One process per GPU: all-gather the exchange regions' IPC handles
+        and map every peer's (cs_tp_attach_ipc)."""
+        import ctypes as C
+        h = (C.c_uint8 * 64)()
+        cs.engine._check(cs.lib().cs_tp_exchange_ipc_handle(eng._h, h))
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(h))
+        allh = (C.c_uint8 * (64 * world)).from_buffer_copy(b"".join(handles))
+        cs.engine._check(cs.lib().cs_tp_attach_ipc(eng._h, allh, world))
+
+    def reduce_max(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
+
     def replay(name, timed=True):
         """Replays tests/golden/<trace> on one engine: W warm-up iterations,
         then the K step slices (timed region: barrier + sync on both sides)."""
@@ -524,13 +563,7 @@ def main():
         t_setup = time.time()
         eng = cs.Engine(cfg)
         if shard:
-            import ctypes as C
-            h = (C.c_uint8 * 64)()
-            cs.engine._check(cs.lib().cs_tp_exchange_ipc_handle(eng._h, h))
-            handles = [None] * world
-            dist.all_gather_object(handles, bytes(h))
-            allh = (C.c_uint8 * (64 * world)).from_buffer_copy(b"".join(handles))
-            cs.engine._check(cs.lib().cs_tp_attach_ipc(eng._h, allh, world))
+            attach_tp(eng)
         setup_s = time.time() - t_setup
         R.run(eng, tr, 0, W)
         s0 = eng.stats()
@@ -564,15 +597,25 @@ def main():
         gpu_ms = cat("gpu_ms")
         step_ms = np.array([p.gpu_ms.sum() for p in parts])
         gpu_s, wall_s = float(gpu_ms.sum()) / 1e3, float(wall_ms.sum()) / 1e3
+        ranks_ckpt = None
         if dist:
             t = torch.tensor([gpu_s, wall_s], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             gpu_s, wall_s = float(t[0]), float(t[1])
+            # per-rank checkpoint traffic: every rank moves its own KV-head shard
+            # over its own host link, concurrently (config 5)
+            mine = torch.tensor([s1.moved_d2h_bytes - s0.moved_d2h_bytes, s1.moved_d2h_ms - s0.moved_d2h_ms,
+                                 s1.moved_h2d_bytes - s0.moved_h2d_bytes, s1.moved_h2d_ms - s0.moved_h2d_ms,
+                                 s1.host_numa_node], dtype=torch.float64, device="cuda")
+            allr = [torch.zeros_like(mine) for _ in range(world)]
+            dist.all_gather(allr, mine)
+            ranks_ckpt = [x.tolist() for x in allr]
         eng.close()
         return dict(tr=tr, W=W, sl=sl, s0=s0, s1=s1, off=off, on=on, tpot=tpot, tbt=tbt, gpu_s=gpu_s, wall_s=wall_s,
                     clocks=clocks, setup_s=setup_s, kt=kt, gpu_ms=gpu_ms, step_ms=step_ms,
                     dropped=cat("dropped_layer"), drop_us=cat("drop_latency_us"), pre_drop=cat("pre_drop_layer_us"),
-                    h2d=cat("h2d_bytes"), d2h=cat("d2h_bytes"), iters=int(sum(p.iterations for p in parts)))
+                    h2d=cat("h2d_bytes"), d2h=cat("d2h_bytes"), iters=int(sum(p.iterations for p in parts)),
+                    ranks_ckpt=ranks_ckpt)
 
     rp = replay(args.workload)
     reps = world if (world > 1 and not tp) else 1
@@ -607,9 +650,13 @@ def main():
         live["margin_0"] = live_leg(args.workload, local, margin=0.0)
 
     probes = {}
+    if not args.no_probes and tp:  # every rank: the agreement cost at g = world
+        probes["safepoint_overhead"] = safepoint_overhead(cs, F, shard=dict(tp_size=world, tp_rank=rank),
+                                                          attach=attach_tp, reduce_max=reduce_max)
     if not args.no_probes and rank == 0:
         probes["attention"] = attention_probe(cs, F, hbm_peak, bf16_peak)
-        probes["safepoint_overhead"] = safepoint_overhead(cs, F)
+        if not tp:
+            probes["safepoint_overhead"] = safepoint_overhead(cs, F)
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -714,7 +761,9 @@ def main():
                     "h2d_gbs": h2d_b / (h2d_ms * 1e-3) / 1e9 if h2d_ms > 0 else None,
                     "d2h_bytes": d2h_b, "h2d_bytes": h2d_b, "host_link_peak_gbs": link_peak,
                     "frac_d2h": (d2h_b / (d2h_ms * 1e-3) / 1e9) / link_peak["d2h"] if d2h_ms > 0 else None,
-                    "frac_h2d": (h2d_b / (h2d_ms * 1e-3) / 1e9) / link_peak["h2d"] if h2d_ms > 0 else None},
+                    "frac_h2d": (h2d_b / (h2d_ms * 1e-3) / 1e9) / link_peak["h2d"] if h2d_ms > 0 else None,
+                    "host_numa_node": s1.host_numa_node,
+                    **ckpt_ranks(rp["ranks_ckpt"])},
         "nonresident_reads": s1.nonresident_reads,
         "legs": legs,
         "live": dict(live, what="live mode (oracle/lockstep/live.cpp): the unmodified reference SimEngine schedules "

@@ -208,6 +208,7 @@ typedef struct {
   int64_t kernel_launches;       /* hand-written kernels launched so far (cuBLAS/NCCL excluded) */
   int64_t host_lru_evicted_pages; /* host copies dropped by the host LRU (kv_cache.cpp:326-362) */
   int64_t unbacked_reads;        /* block-table reads past a request's pages (reference defect D5) */
+  int32_t host_numa_node;        /* NUMA node the pinned host pool is bound to (-1: not bound) */
 } cs_kv_stats;
 int cs_kv_stats_get(cs_engine* e, cs_kv_stats* out);
 int cs_kv_request_info(cs_engine* e, int64_t id, int64_t* gpu_pages, int64_t* covered_tokens,

@@ -85,7 +85,7 @@ class cs_kv_stats(C.Structure):
         ("quarantined_blocks", C.c_int64), ("n_host_slots", C.c_int64), ("free_host_slots", C.c_int64),
         ("moved_d2h_bytes", C.c_int64), ("moved_h2d_bytes", C.c_int64), ("nonresident_reads", C.c_int64),
         ("moved_d2h_ms", C.c_double), ("moved_h2d_ms", C.c_double), ("kernel_launches", C.c_int64),
-        ("host_lru_evicted_pages", C.c_int64), ("unbacked_reads", C.c_int64),
+        ("host_lru_evicted_pages", C.c_int64), ("unbacked_reads", C.c_int64), ("host_numa_node", C.c_int32),
     ]
 
 

@@ -116,7 +116,9 @@ struct P2PArgs {
   const __nv_bfloat16* part[8];
   uint64_t* flag[8];   // published step of each rank
   uint64_t* step[8];   // step counter of each rank (only step[rank] is used)
+  uint64_t* flag2[8];  // two-shot: reduce-scatter phase published by each rank
   int* arrive;         // this rank's block-arrival counter
+  int* arrive2;        // two-shot: this rank's reduce-scatter arrival counter
   int32_t rank, g;
 };
 

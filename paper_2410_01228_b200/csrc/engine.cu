@@ -13,7 +13,12 @@
 #include <nccl.h>
 #include <time.h>
 
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <cctype>
 #include <cmath>
 #include <array>
 #include <atomic>
@@ -22,6 +27,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <fstream>
 #include <functional>
 #include <map>
 #include <memory>
@@ -68,6 +74,7 @@ bool wgemm_supported(int M, int N, int K);
 void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, int Mp, int N, int K, int splits,
               int stages, bool f32_out, cudaStream_t s);
 void p2p_allreduce(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s);
+void p2p_allreduce2(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s);
 bool gemm_pf_supported(int N, int K);
 void gemm_pf(const CUtensorMap* xmap, const CUtensorMap* wmap, void* y, int M, const int32_t* m_dev, int N, int K,
              bool f32_out, int sms, cudaStream_t s, bool swiglu = false);
@@ -236,6 +243,8 @@ struct cs_engine {
   alignas(64) CUtensorMap kv_map{};  // TMA view of the pool as [rows][D] bf16, 64x16 boxes, 128-B swizzle
   __nv_bfloat16* host_kv = nullptr;      // pinned
   __nv_bfloat16* host_kv_dev = nullptr;  // mapped alias
+  size_t host_kv_bytes = 0;
+  int host_numa_node = -1;               // node the pool is bound to, -1 = cudaHostAlloc
   void* weight_mem = nullptr;
   Weights w;
   __nv_bfloat16 *x = nullptr, *xn = nullptr, *qkv = nullptr, *attn = nullptr, *tmp = nullptr, *gu = nullptr,
@@ -291,6 +300,7 @@ struct cs_engine {
   __nv_bfloat16* stage[2] = {nullptr, nullptr};
   size_t stage_elems = 0;
   bool kv_zerocopy = false;  // CS_KV_ZEROCOPY=1: SM zero-copy kernel instead (A/B)
+  bool kv_small_zc = true;  // short-run chunks as one zero-copy kernel (CS_KV_SMALL_ZC=0: off)
   double moved_ms[2] = {0, 0};
   std::atomic<int64_t> launches{0};  // hand-written kernel launches (not cuBLAS/NCCL)
 
@@ -381,6 +391,7 @@ struct cs_engine {
   size_t xchg_part_elems = 0;
   bool p2p = false;
   int p2p_blocks = 0;
+  int p2p_mode = 0;                    // 0 auto, 1 one-shot, 2 two-shot (CS_P2P_ALLREDUCE)
   int part_slot = 0;                   // next partial buffer (same sequence on every rank)
   std::vector<uint8_t*> peer_xchg;     // exchange region of every rank, rank order
   std::vector<cudaIpcMemHandle_t> opened;  // (for cs_destroy) handles we opened
@@ -465,6 +476,15 @@ int64_t DeviceMover::launch(int dir, const std::vector<csb::Segment>& segs, int6
       }
       const void* dseg = ring.dev + off;
       const int64_t* dso = reinterpret_cast<const int64_t*>(ring.dev + off + n * sizeof(csb::Segment));
+      // many short host runs (decode deltas: one 128 KB token per request)
+      // cost a DMA setup each; such a chunk moves as one zero-copy kernel
+      // straight between the blocks and the mapped host slots instead
+      if (e->kv_small_zc && sizes.size() >= 8 && pos * 2 / sizes.size() < (1u << 20)) {
+        csk::kv_move(dir == CS_D2H, e->kv, e->host_kv_dev, dseg, static_cast<int>(n), runs, e->D, e->sms, st);
+        e->launches += 1;
+        i0 = i1;
+        continue;
+      }
       if (dir == CS_D2H) {
         csk::kv_pack(true, e->kv, e->stage[dir], dseg, dso, static_cast<int>(n), runs, e->D, e->sms, st);
         e->launches += 1;
@@ -525,6 +545,67 @@ void validate(const cs_config& c) {
   if (c.gpu_kv_capacity < 1 || c.host_kv_capacity < 1) throw ConfigError("KV capacities must be positive");
   if (c.d2h_bandwidth <= 0 || c.h2d_bandwidth <= 0) throw ConfigError("transfer bandwidths must be positive");
   if (c.max_batched_tokens < 1) throw ConfigError("max_batched_tokens must be >= 1");
+}
+
+// Pinned host KV pool on the GPU's own NUMA node (config 5: 8 ranks each
+// checkpointing over their own host link). The node comes from sysfs for
+// the device's PCI bus id; with more than one node the region is mmap'ed,
+// bound to that node (mbind, MPOL_BIND) before any page is touched, then
+// pinned and mapped for the device (cudaHostRegister). One node, an unknown
+// node or CS_HOST_NUMA=0: plain cudaHostAlloc. *node = the bound node or -1.
+int gpu_numa_node(int device) {
+  char bus[64] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), device) != cudaSuccess) return -1;
+  std::string id(bus);
+  for (char& c : id) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+  if (id.size() > 12) id = id.substr(id.size() - 12);  // dddd:bb:dd.f
+  std::ifstream f("/sys/bus/pci/devices/" + id + "/numa_node");
+  int node = -1;
+  if (!(f >> node)) return -1;
+  return node;
+}
+
+int numa_node_count() {
+  int n = 0;
+  for (int i = 0; i < 1024; ++i) {
+    std::ifstream f("/sys/devices/system/node/node" + std::to_string(i) + "/cpulist");
+    if (!f) break;
+    ++n;
+  }
+  return n;
+}
+
+void* alloc_host_pool(int device, size_t bytes, int* node) {
+  *node = -1;
+  const char* env = std::getenv("CS_HOST_NUMA");
+  const int want = env && env[0] == '0' ? -1 : gpu_numa_node(device);
+  if (want >= 0 && want < 64 && numa_node_count() > 1) {
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p != MAP_FAILED) {
+      unsigned long mask = 1ul << want;
+      constexpr int kMpolBind = 2;
+      if (syscall(SYS_mbind, p, bytes, kMpolBind, &mask, 64, 0) == 0 &&
+          cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable) == cudaSuccess) {
+        *node = want;
+        return p;
+      }
+      cudaGetLastError();  // clear a failed registration; fall back below
+      munmap(p, bytes);
+    }
+  }
+  void* p = nullptr;
+  CK(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  return p;
+}
+
+void free_host_pool(void* p, size_t bytes, int node) {
+  if (!p) return;
+  if (node >= 0) {
+    cudaHostUnregister(p);
+    munmap(p, bytes);
+  } else {
+    cudaFreeHost(p);
+  }
 }
 
 // TMA descriptor for the KV pool viewed as [rows][D] bf16 (a page of one
@@ -791,11 +872,21 @@ void cs_engine::reduce_into(__nv_bfloat16* buf, int64_t count) {
     a.part[r] = xpart(peer_xchg[static_cast<size_t>(r)], part_slot);
     a.flag[r] = xflag(peer_xchg[static_cast<size_t>(r)]);
     a.step[r] = xflag(peer_xchg[static_cast<size_t>(r)]) + 1;
+    a.flag2[r] = xflag(peer_xchg[static_cast<size_t>(r)]) + 3;
   }
   a.arrive = reinterpret_cast<int*>(xflag(xchg) + 2);
+  a.arrive2 = reinterpret_cast<int*>(xflag(xchg) + 4);
   a.rank = rank;
   a.g = tp;
-  csk::p2p_allreduce(a, buf, count, p2p_blocks, s_compute);
+  // two-shot (reduce-scatter + all-gather, 2(g-1)/g x payload over NVLink
+  // per rank) for large payloads at g >= 4; one-shot ((g-1) x payload, one
+  // barrier) otherwise. CS_P2P_ALLREDUCE=oneshot|twoshot forces either.
+  const bool two = p2p_mode == 2 || (p2p_mode == 0 && tp >= 4 && count * 2 >= (512 << 10));
+  if (two) {
+    csk::p2p_allreduce2(a, buf, count, p2p_blocks, s_compute);
+  } else {
+    csk::p2p_allreduce(a, buf, count, p2p_blocks, s_compute);
+  }
   part_slot ^= 1;
 }
 
@@ -1315,12 +1406,14 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
       CK(cudaMalloc(&e->kv, static_cast<size_t>(pc.n_blocks + 1) * blk_bytes));
       CK(cudaMemset(e->kv, 0, static_cast<size_t>(pc.n_blocks + 1) * blk_bytes));  // finite everywhere
       make_kv_tensor_map(&e->kv_map, e->kv, static_cast<uint64_t>(pc.n_blocks + 1) * e->L * 2 * e->hkv * 16, e->D);
-      CK(cudaHostAlloc(&e->host_kv, static_cast<size_t>(pc.n_slots) * blk_bytes,
-                       cudaHostAllocMapped | cudaHostAllocPortable));
+      e->host_kv_bytes = static_cast<size_t>(pc.n_slots) * blk_bytes;
+      e->host_kv = static_cast<__nv_bfloat16*>(alloc_host_pool(cfg->device, e->host_kv_bytes, &e->host_numa_node));
       CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->host_kv_dev), e->host_kv, 0));
       {
         const char* zc = std::getenv("CS_KV_ZEROCOPY");
         e->kv_zerocopy = zc && zc[0] == '1';
+        const char* sz = std::getenv("CS_KV_SMALL_ZC");
+        e->kv_small_zc = !(sz && sz[0] == '0');
         if (!e->kv_zerocopy) {
           // 256 MiB per direction (>= one page): a larger job runs as a
           // sequence of pack + DMA chunks on its stream
@@ -1519,7 +1612,7 @@ int cs_destroy(cs_engine* e) {
       for (void* p : e->opened_ptrs) cudaIpcCloseMemHandle(p);
       if (e->xchg) cudaFree(e->xchg);
       cudaFree(e->kv);
-      cudaFreeHost(e->host_kv);
+      free_host_pool(e->host_kv, e->host_kv_bytes, e->host_numa_node);
       for (int d = 0; d < 2; ++d)
         if (e->stage[d]) cudaFree(e->stage[d]);
       for (auto& r : e->ring) cudaFreeHost(r.host);
@@ -1592,6 +1685,9 @@ static void attach_common(cs_engine* e, const std::vector<uint8_t*>& peers, bool
   // same-device (loopback) peers run concurrently with this kernel's
   // spinning blocks: keep it small so the other rank's kernels get SMs
   e->p2p_blocks = same_device ? 16 : 2 * e->sms;
+  if (const char* m = std::getenv("CS_P2P_ALLREDUCE")) {
+    e->p2p_mode = std::strcmp(m, "twoshot") == 0 ? 2 : std::strcmp(m, "oneshot") == 0 ? 1 : 0;
+  }
   e->drop_graphs();
 }
 
@@ -1758,6 +1854,7 @@ int cs_kv_stats_get(cs_engine* e, cs_kv_stats* o) {
     o->nonresident_reads = p.nonresident_reads();
     o->host_lru_evicted_pages = p.host_lru_evicted();
     o->unbacked_reads = p.unbacked_reads();
+    o->host_numa_node = e->host_numa_node;
     o->moved_d2h_ms = e->moved_ms[CS_D2H];
     o->kernel_launches = e->launches.load();
     o->moved_h2d_ms = e->moved_ms[CS_H2D];

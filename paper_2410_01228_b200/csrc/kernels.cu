@@ -581,6 +581,105 @@ __global__ void __launch_bounds__(256) p2p_allreduce_kernel(P2PArgs a, __nv_bflo
   }
 }
 
+// Two-shot variant for large payloads (reduce-scatter + all-gather over peer
+// memory). Rank r owns vector chunk r of the buffer: after the same flag
+// handshake it sums chunk r of the g partials in fp32 and writes the bf16 sum
+// back IN PLACE into its own partial (peers read only their own chunks of it
+// in this phase); the blocks then meet at a second, grid-wide barrier that
+// publishes flag2[rank]; once every rank's flag2 reaches seq, every block
+// copies chunk p of rank p's (now reduced) partial into out. Remote bytes per
+// rank: 2 (g-1)/g x payload instead of (g-1) x payload for the one-shot
+// kernel; the fp32 summation order (rank 0..g-1) is the same, so both kernels
+// produce bit-identical sums. Requires all blocks co-resident (grid <= SMs x
+// resident blocks), as the one-shot flag wait already does.
+__device__ __forceinline__ void p2p_wait_all(const P2PArgs& a, uint64_t* const* flags, uint64_t seq,
+                                             const char* what) {
+  if (threadIdx.x < a.g) {
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_sys(flags[threadIdx.x]) < seq) {
+      if (globaltimer_ns() - t0 > 2000000000ull) {
+        printf("p2p_allreduce2: rank %d timed out in %s waiting for rank %d (seq %llu)\n", a.rank, what,
+               threadIdx.x, static_cast<unsigned long long>(seq));
+        __trap();
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) p2p_allreduce2_kernel(P2PArgs a, __nv_bfloat16* out, int64_t count) {
+  __shared__ uint64_t s_seq;
+  __shared__ int s_last;
+  if (threadIdx.x == 0) s_seq = *reinterpret_cast<volatile uint64_t*>(a.step[a.rank]) + 1;
+  __syncthreads();
+  const uint64_t seq = s_seq;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(a.flag[a.rank], seq);
+  }
+  p2p_wait_all(a, a.flag, seq, "phase 0");
+  const int64_t nv = count / 8;
+  const int64_t per = (nv + a.g - 1) / a.g;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  // phase 1: reduce-scatter, own chunk in place
+  {
+    uint4* mine = reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(a.part[a.rank]));
+    const int64_t v1 = min(nv, (a.rank + 1) * per);
+    for (int64_t i = a.rank * per + tid; i < v1; i += stride) {
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int p = 0; p < a.g; ++p) {
+        const uint4 v = __ldcv(reinterpret_cast<const uint4*>(a.part[p]) + i);
+        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(e[j]);
+      }
+      uint4 o;
+      __nv_bfloat16* oe = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) oe[j] = __float2bfloat16(acc[j]);
+      __stcg(mine + i, o);
+    }
+    if (a.rank == a.g - 1 && blockIdx.x == 0) {  // tail (count % 8) belongs to the last rank
+      __nv_bfloat16* m = const_cast<__nv_bfloat16*>(a.part[a.rank]);
+      for (int64_t i = nv * 8 + threadIdx.x; i < count; i += blockDim.x) {
+        float acc = 0.f;
+        for (int p = 0; p < a.g; ++p) acc += __bfloat162float(a.part[p][i]);
+        m[i] = __float2bfloat16(acc);
+      }
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(a.arrive2, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    *a.arrive2 = 0;
+    __threadfence_system();
+    st_release_sys(a.flag2[a.rank], seq);
+  }
+  p2p_wait_all(a, a.flag2, seq, "phase 1");
+  // phase 2: all-gather of the reduced chunks
+  for (int64_t i = tid; i < nv; i += stride) {
+    const int owner = static_cast<int>(i / per);
+    reinterpret_cast<uint4*>(out)[i] = __ldcv(reinterpret_cast<const uint4*>(a.part[owner]) + i);
+  }
+  if (blockIdx.x == 0) {
+    for (int64_t i = nv * 8 + threadIdx.x; i < count; i += blockDim.x) out[i] = a.part[a.g - 1][i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(a.arrive, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    *a.arrive = 0;
+    *reinterpret_cast<volatile uint64_t*>(a.step[a.rank]) = seq;
+  }
+}
+
+void p2p_allreduce2(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s) {
+  p2p_allreduce2_kernel<<<blocks, 256, 0, s>>>(a, out, count);
+}
+
 void p2p_allreduce(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s) {
   if (count <= 0) return;
   p2p_allreduce_kernel<<<blocks, 256, 0, s>>>(a, out, count);

@@ -60,3 +60,16 @@ def test_percentile_is_nearest_rank():
     assert bench.percentile(xs, 0.5) == 3.0
     assert bench.percentile(xs, 0.2) == 1.0
     assert bench.percentile([], 0.99) == 0.0
+
+
+def test_ckpt_ranks_aggregate_is_bytes_over_slowest_rank():
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.ckpt_ranks(None) == {}
+    rows = [[4e9, 100.0, 2e9, 50.0, 0], [4e9, 80.0, 2e9, 40.0, 1]]
+    d = bench.ckpt_ranks(rows)
+    assert [r["rank"] for r in d["per_rank"]] == [0, 1]
+    assert abs(d["per_rank"][1]["d2h_gbs"] - 50.0) < 1e-9
+    assert abs(d["aggregate_d2h_gbs"] - 80.0) < 1e-9   # 8 GB over the slower rank's 100 ms
+    assert abs(d["aggregate_h2d_gbs"] - 80.0) < 1e-9
+    assert d["per_rank"][1]["host_numa_node"] == 1

@@ -30,11 +30,11 @@ pytestmark = pytest.mark.gpu
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _in_child(case):
+def _in_child(case, tp=2, mode="auto"):
     root = os.path.dirname(_HERE)
-    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER",
+    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER", CS_P2P_ALLREDUCE=mode,
                PYTHONPATH=os.pathsep.join([root, os.environ.get("PYTHONPATH", "")]))
-    p = subprocess.Popen([sys.executable, os.path.abspath(__file__), case], env=env, stdout=subprocess.PIPE,
+    p = subprocess.Popen([sys.executable, os.path.abspath(__file__), case, str(tp)], env=env, stdout=subprocess.PIPE,
                          stderr=subprocess.STDOUT, text=True, cwd=os.path.dirname(_HERE))
     try:
         out = p.communicate(timeout=420)[0]
@@ -49,18 +49,18 @@ SHAPE = dict(num_layers=4, hidden=256, n_heads=8, n_kv_heads=4, head_dim=64, ffn
              max_batched_tokens=1024, gpu_kv_capacity=4096 * 16 * 2 * 4 * 64 * 2 * 4, safepoint_interval_layers=1)
 
 
-def _engines(instrumented=0):
+def _engines(instrumented=0, tp=2):
     full = cs.Engine(cs.model_config("tiny", instrumented=instrumented, **SHAPE))
-    ranks = [cs.Engine(cs.model_config("tiny", instrumented=instrumented, tp_size=2, tp_rank=r, **SHAPE))
-             for r in range(2)]
+    ranks = [cs.Engine(cs.model_config("tiny", instrumented=instrumented, tp_size=tp, tp_rank=r, **SHAPE))
+             for r in range(tp)]
     ptrs = []
     for e in ranks:
         p = C.c_void_p()
         cs.engine._check(cs.lib().cs_tp_exchange_ptr(e._h, C.byref(p)))
         ptrs.append(p.value)
-    arr = (C.c_void_p * 2)(*ptrs)
+    arr = (C.c_void_p * tp)(*ptrs)
     for e in ranks:
-        cs.engine._check(cs.lib().cs_tp_attach_peers(e._h, arr, 2, 1))
+        cs.engine._check(cs.lib().cs_tp_attach_peers(e._h, arr, tp, 1))
     return full, ranks
 
 
@@ -87,8 +87,19 @@ def test_flag_on_one_rank_drops_both_at_the_same_layer():
     _in_child("flag")
 
 
-def case_match():
-    full, ranks = _engines()
+@pytest.mark.parametrize("tp,mode", [(2, "twoshot"), (4, "oneshot"), (4, "twoshot")])
+def test_ranks_match_unsharded_per_allreduce_kernel(tp, mode):
+    """The two-shot (reduce-scatter + all-gather) peer kernel gives the same
+    bits as the one-shot kernel's fold order; tp=4 exercises uneven chunks."""
+    _in_child("match", tp, mode)
+
+
+def test_flag_on_one_rank_drops_all_four_twoshot():
+    _in_child("flag", 4, "twoshot")
+
+
+def case_match(tp=2):
+    full, ranks = _engines(tp=tp)
     engs = [full] + ranks
     orc = N.Oracle(N.ModelShape.from_cfg(full.cfg))
     try:
@@ -110,8 +121,9 @@ def case_match():
             outs = _step(engs, plan, allocs, 100 + it)
             print(f"iteration {it} done", flush=True)
             ref = orc.forward([N.Entry(b.request_id, b.compute_tokens, b.context_tokens, b.kind, b.online) for b in plan])
-            (_, lf), (_, l0), (_, l1) = outs
-            assert np.array_equal(l0, l1)                  # ranks agree exactly
+            (_, lf), (_, l0) = outs[0], outs[1]
+            for _, lr in outs[2:]:
+                assert np.array_equal(l0, lr)              # ranks agree exactly
             assert float(np.max(np.abs(l0 - lf))) <= 2e-2  # sharded vs unsharded (bf16 partial sums)
             assert float(np.max(np.abs(l0 - ref))) <= 2e-2
             for e in engs:
@@ -124,18 +136,20 @@ def case_match():
             e.close()
 
 
-def case_flag():
-    full, ranks = _engines(instrumented=1)
+def case_flag(tp=2):
+    full, ranks = _engines(instrumented=1, tp=tp)
     full.close()
     try:
         for e in ranks:
             e.register_request(0, True)
             e.register_request(1, False)
         plan = [cs.BatchEntry(0, 30, 0, cs.CS_PREFILL, True), cs.BatchEntry(1, 900, 0, cs.CS_PREFILL, False)]
-        (i0, _), (i1, _) = _step(ranks, plan, [31, 900], 7, signal_rank=0)
-        assert i0.preempted_at_layer == i1.preempted_at_layer
-        if i0.preempted_at_layer is not None:
-            assert i0.n_outputs == i1.n_outputs == 1
+        infos = [i for i, _ in _step(ranks, plan, [31, 900], 7, signal_rank=0)]
+        i0 = infos[0]
+        for i1 in infos[1:]:
+            assert i0.preempted_at_layer == i1.preempted_at_layer
+            if i0.preempted_at_layer is not None:
+                assert i0.n_outputs == i1.n_outputs == 1
         for e in ranks:
             e.commit_allocations(0)
             if i0.preempted_at_layer is not None:
@@ -152,5 +166,5 @@ if __name__ == "__main__":
     import faulthandler
     faulthandler.dump_traceback_later(360, exit=True)  # a hang prints every thread's stack
     sys.path.insert(0, os.path.dirname(_HERE))
-    {"match": case_match, "flag": case_flag}[sys.argv[1]]()
+    {"match": case_match, "flag": case_flag}[sys.argv[1]](int(sys.argv[2]) if len(sys.argv) > 2 else 2)
     print("ok")

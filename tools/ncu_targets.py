@@ -65,6 +65,7 @@ def gather(n_blocks=1024):
     eng.note_written(0, 0, n_blocks * 16)
     eng.stage_checkpoint(0, 0, n_blocks * 16)
     job = eng.flush_checkpoints(0)
+    eng.job_wait(job.id)
     eng.on_transfer_done(job.id, job.done_time)
     s = eng.stats()
     print(f"gather: {s.moved_d2h_bytes} B in {s.moved_d2h_ms:.3f} ms = {s.moved_d2h_bytes / s.moved_d2h_ms / 1e6:.1f} GB/s")
