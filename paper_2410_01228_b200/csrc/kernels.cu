@@ -81,10 +81,16 @@ __device__ __forceinline__ void apply_drop(IterDesc* desc, PreemptMailbox* mb, i
 __device__ __forceinline__ void safepoint_check(IterDesc* desc, const SafepointArg& sp) {
   if (sp.mb == nullptr) return;
   if (sp.layer == 0) desc->start_ns = globaltimer_ns();
+  // the flag is read BEFORE this layer's progress is published: a host that
+  // stores the flag on seeing layer l (the reference's Alg. 1 firing inside
+  // layer l) must land the drop at layer l + 1, never at l itself (the read
+  // would otherwise race the host's reaction to the progress write)
+  const uint64_t flag = sp.mb->flag_epoch;
+  __threadfence_system();
   sp.mb->progress = desc->epoch * 1024ull + static_cast<uint64_t>(sp.layer);
   if (sp.mode == 0 || desc->dropped_at >= 0) return;
   if (sp.mode == 1) {
-    if (sp.mb->flag_epoch != desc->epoch) return;
+    if (flag != desc->epoch) return;
     if (desc->n_ent_on >= desc->n_ent_cur) return;  // nothing offline to drop
   } else if (__bfloat162float(sp.tail[0]) <= 0.f) {
     return;

@@ -1,12 +1,14 @@
 """GPU parity of the layer forward (K1 decode attention, K2 prefill attention,
 K3 RoPE + KV append, norms, GEMMs, lm_head) against the CPU oracle, through
 the C-ABI. Tolerances (bf16 engine vs fp32 oracle with bf16 storage points):
-attention output rel-L2 <= 1e-2, logits max-abs <= 2e-2."""
+attention output rel-L2 <= 1e-2; logits max-abs <= min(2e-2, 0.06 x std of
+the oracle logits); argmax agreement >= 99% on rows whose oracle top-2 gap
+exceeds twice that bound (helpers.logit_bound / decisive_rows)."""
 import numpy as np
 import pytest
 
 import paper_2410_01228_b200 as cs
-from helpers import Driver, rel_l2
+from helpers import DECISIVE_AGREE, Driver, decisive_rows, logit_bound, rel_l2
 
 pytestmark = pytest.mark.gpu
 
@@ -18,9 +20,10 @@ def _check(drv, info, logits, ref, attn_rows=None):
     assert ref is not None
     assert logits.shape == ref.shape
     err = float(np.max(np.abs(logits - ref)))
-    assert err <= LOGIT_TOL, err
-    agree = np.mean(np.argmax(logits, -1) == np.argmax(ref, -1))
-    assert agree >= 0.9, agree
+    bound = logit_bound(ref)
+    assert err <= bound, (err, bound)
+    ok, dec = decisive_rows(logits, ref, bound)
+    assert ok >= DECISIVE_AGREE * dec, (ok, dec)
     if attn_rows is not None:
         c = drv.cfg
         got = drv.eng.read_activation(0, attn_rows, c.n_heads * c.head_dim)
