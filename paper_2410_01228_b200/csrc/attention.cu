@@ -265,6 +265,260 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
   if (threadIdx.x == 0) *cnt = 0;
 }
 
+// ---------------------------------------------------------- K1 stream-K ----
+// The decode work is (entry, KV head) pairs x their pages. A fixed grid of
+// `gridDim.x` CTAs (all resident: the occupancy limit x SMs) splits the
+// flattened page sequence of ALL pairs into equal contiguous ranges of W
+// pages, so every CTA streams the same number of K/V bytes whatever the mix
+// of context lengths -- no wave tail, no idle SMs on a 39-sequence step. A
+// CTA walks the pair segments of its range; a pair covered by one CTA is
+// written directly, a pair cut by range boundaries leaves one fp32 partial
+// (m, l, O) per covering CTA (slot 0 = the CTA's first segment, slot 1 = its
+// last) and the last covering CTA to finish folds them (per-pair arrival
+// counter, self-resetting). W and the pair layout come from the device
+// descriptor (n_dec_cur) and the page prefix sums, so a captured graph serves
+// every plan of its bucket and a safepoint drop re-balances the next layer.
+template <int D, int G>
+__global__ void __launch_bounds__(128, 3) attn_decode_sk_kernel(AttnParams p) {
+  pdl_trigger();
+  constexpr int KS = D / 16;
+  constexpr int NTD = D / 8;
+  constexpr int PB = kPage * D * 2;  // bytes per K (or V) page
+  constexpr int kMinPages = 16;      // >= 4 pages per warp
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ int s_last;
+  const int n_dec = p.desc->n_dec_cur;
+  if (n_dec <= 0) return;
+  const int hkv = p.hkv;
+  const int total = hkv * p.dec_pfx[n_dec];
+  const int W = max(kMinPages, (total + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x));
+  const int c = blockIdx.x;
+  const int g_begin = c * W;
+  const int g_end = min(total, g_begin + W);
+  if (g_begin >= g_end) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  constexpr int kPart = G * (D + 2);  // floats per partial: m[G], l[G], O[G][D]
+
+  // first decode entry of the range: largest i with hkv * pfx[i] <= g_begin
+  int i;
+  {
+    int lo = 0, hi = n_dec - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (hkv * p.dec_pfx[mid] <= g_begin) lo = mid; else hi = mid - 1;
+    }
+    i = lo;
+  }
+  int g = g_begin;
+  while (g < g_end) {
+    while (hkv * p.dec_pfx[i + 1] <= g) ++i;
+    const int n_i = p.dec_pfx[i + 1] - p.dec_pfx[i];
+    const int base_i = hkv * p.dec_pfx[i];
+    const int kvh = (g - base_i) / n_i;
+    const int P = base_i + kvh * n_i;  // this pair's first global page
+    const int seg_end = min(g_end, P + n_i);
+    const int pg0 = g - P, pg1 = seg_end - P;
+    const bool first_seg = g == g_begin;
+    g = seg_end;
+
+    const int ent = p.dec_ent[i];
+    const int row = p.ent_q0[ent];
+    const int kv_len = p.ent_kvlen[ent];
+    const int32_t* bt = p.block_table + p.ent_bt[ent];
+
+    uint32_t qa[KS][4];
+    {
+      const __nv_bfloat16* q = p.qkv + static_cast<size_t>(row) * p.qkv_stride + static_cast<size_t>(kvh) * G * D;
+      const int r0 = gid, r1 = gid + 8;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int d0 = ks * 16 + tig * 2;
+        qa[ks][0] = r0 < G ? *reinterpret_cast<const uint32_t*>(q + r0 * D + d0) : 0u;
+        qa[ks][1] = r1 < G ? *reinterpret_cast<const uint32_t*>(q + r1 * D + d0) : 0u;
+        qa[ks][2] = r0 < G ? *reinterpret_cast<const uint32_t*>(q + r0 * D + d0 + 8) : 0u;
+        qa[ks][3] = r1 < G ? *reinterpret_cast<const uint32_t*>(q + r1 * D + d0 + 8) : 0u;
+      }
+    }
+    float o[NTD][4];
+#pragma unroll
+    for (int k = 0; k < NTD; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+    uint8_t* wbuf = smem + warp * 4 * PB;  // [stage][K|V]
+    int pg = pg0 + warp;
+    if (pg < pg1) {
+      load_page_async<D>(wbuf, wbuf + PB, kv_page(p, bt[pg], kvh, 0, D), kv_page(p, bt[pg], kvh, 1, D), lane);
+    }
+    cp_async_commit();
+    int stage = 0;
+    for (; pg < pg1; pg += 4) {
+      const int nxt = pg + 4;
+      if (nxt < pg1) {
+        uint8_t* nb = wbuf + (stage ^ 1) * 2 * PB;
+        load_page_async<D>(nb, nb + PB, kv_page(p, bt[nxt], kvh, 0, D), kv_page(p, bt[nxt], kvh, 1, D), lane);
+      }
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp();
+      const uint8_t* sK = wbuf + stage * 2 * PB;
+      const uint8_t* sV = sK + PB;
+      float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int mi = lane >> 3;
+        const int tok = (mi >> 1) * 8 + (lane & 7);
+        uint32_t b0, b1, b2, b3;
+        ldmatrix_x4(b0, b1, b2, b3, sK + swz<D>(tok, ks * 2 + (mi & 1)));
+        mma_bf16_16816(sc[0], qa[ks], b0, b1);
+        mma_bf16_16816(sc[1], qa[ks], b2, b3);
+      }
+      const int base = pg * kPage;
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const bool ok = base + nt * 8 + tig * 2 + j < kv_len;
+          sc[nt][j] = ok ? sc[nt][j] * p.scale_log2 : -INFINITY;
+          sc[nt][2 + j] = ok ? sc[nt][2 + j] * p.scale_log2 : -INFINITY;
+          mx0 = fmaxf(mx0, sc[nt][j]);
+          mx1 = fmaxf(mx1, sc[nt][2 + j]);
+        }
+      }
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
+      m0 = mn0;
+      m1 = mn1;
+      uint32_t pa[4];
+      float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const float p0 = exp2f(sc[nt][0] - mn0), p1 = exp2f(sc[nt][1] - mn0);
+        const float p2 = exp2f(sc[nt][2] - mn1), p3 = exp2f(sc[nt][3] - mn1);
+        rs0 += p0 + p1;
+        rs1 += p2 + p3;
+        pa[nt * 2 + 0] = pack_bf16(p0, p1);
+        pa[nt * 2 + 1] = pack_bf16(p2, p3);
+      }
+      l0 = l0 * al0 + rs0;
+      l1 = l1 * al1 + rs1;
+#pragma unroll
+      for (int k = 0; k < NTD; ++k) {
+        o[k][0] *= al0;
+        o[k][1] *= al0;
+        o[k][2] *= al1;
+        o[k][3] *= al1;
+      }
+#pragma unroll
+      for (int nd = 0; nd < D / 16; ++nd) {
+        const int mi = lane >> 3;
+        const int tok = (mi & 1) * 8 + (lane & 7);
+        uint32_t v0, v1, v2, v3;
+        ldmatrix_x4_trans(v0, v1, v2, v3, sV + swz<D>(tok, nd * 2 + (mi >> 1)));
+        mma_bf16_16816(o[nd * 2], pa, v0, v1);
+        mma_bf16_16816(o[nd * 2 + 1], pa, v2, v3);
+      }
+      __syncwarp();
+      stage ^= 1;
+    }
+    cp_async_wait<0>();
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+
+    // merge the 4 warps in smem (aliases the K/V ring: all warps are done)
+    __syncthreads();
+    float* sm_m = reinterpret_cast<float*>(smem);
+    float* sm_l = sm_m + 4 * 16;
+    float* sm_o = sm_l + 4 * 16;
+    if (tig == 0) {
+      sm_m[warp * 16 + gid] = m0;
+      sm_m[warp * 16 + gid + 8] = m1;
+      sm_l[warp * 16 + gid] = l0;
+      sm_l[warp * 16 + gid + 8] = l1;
+    }
+#pragma unroll
+    for (int nt = 0; nt < NTD; ++nt) {
+      const int d = nt * 8 + tig * 2;
+      sm_o[(warp * 16 + gid) * D + d] = o[nt][0];
+      sm_o[(warp * 16 + gid) * D + d + 1] = o[nt][1];
+      sm_o[(warp * 16 + gid + 8) * D + d] = o[nt][2];
+      sm_o[(warp * 16 + gid + 8) * D + d + 1] = o[nt][3];
+    }
+    __syncthreads();
+    const bool full = pg0 == 0 && pg1 == n_i;
+    float* part = p.ws_sk + (static_cast<size_t>(c) * 2 + (first_seg ? 0 : 1)) * kPart;
+    for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+      const int r = idx / D, d = idx % D;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w * 16 + r]);
+      float L = 0.f, O = 0.f;
+      if (M != -INFINITY) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const float f = exp2f(sm_m[w * 16 + r] - M);
+          L += sm_l[w * 16 + r] * f;
+          O += sm_o[(w * 16 + r) * D + d] * f;
+        }
+      }
+      if (full) {
+        p.out[static_cast<size_t>(row) * p.hq * D + static_cast<size_t>(kvh * G + r) * D + d] =
+            __float2bfloat16(L > 0.f ? O / L : 0.f);
+      } else {
+        if (d == 0) {
+          part[r] = M;
+          part[G + r] = L;
+        }
+        part[2 * G + r * D + d] = O;
+      }
+    }
+    if (!full) {
+      // the last of the pair's covering CTAs folds their partials
+      const int c_first = P / W, c_last = (P + n_i - 1) / W;
+      __threadfence();
+      __syncthreads();
+      int32_t* cnt = p.dec_cnt + static_cast<size_t>(i) * hkv + kvh;
+      if (threadIdx.x == 0) s_last = atomicAdd(cnt, 1) == c_last - c_first;
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        const int nseg = c_last - c_first + 1;
+        for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+          const int r = idx / D, d = idx % D;
+          float M = -INFINITY;
+          for (int k = 0; k < nseg; ++k) {
+            const int cc = c_first + k;
+            const float* pp = p.ws_sk + (static_cast<size_t>(cc) * 2 + (cc * W >= P ? 0 : 1)) * kPart;
+            M = fmaxf(M, __ldcg(pp + r));
+          }
+          float L = 0.f, O = 0.f;
+          if (M != -INFINITY) {
+            for (int k = 0; k < nseg; ++k) {
+              const int cc = c_first + k;
+              const float* pp = p.ws_sk + (static_cast<size_t>(cc) * 2 + (cc * W >= P ? 0 : 1)) * kPart;
+              const float ms = __ldcg(pp + r);
+              const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
+              L += __ldcg(pp + G + r) * f;
+              O += __ldcg(pp + 2 * G + r * D + d) * f;
+            }
+          }
+          p.out[static_cast<size_t>(row) * p.hq * D + static_cast<size_t>(kvh * G + r) * D + d] =
+              __float2bfloat16(L > 0.f ? O / L : 0.f);
+        }
+        if (threadIdx.x == 0) *cnt = 0;
+      }
+    }
+    __syncthreads();  // smem (merge scratch = K/V ring) is free for the next segment
+  }
+}
+
 // ------------------------------------------------------------- launchers ----
 int decode_smem_bytes(int D) { return 4 * 4 * kPage * D * 2 > (4 * 16 * 2 + 4 * 16 * D) * 4 ? 4 * 4 * kPage * D * 2 : (4 * 16 * 2 + 4 * 16 * D) * 4; }
 
@@ -276,11 +530,37 @@ static void launch_attention_t(const AttnParams& p, const CUtensorMap* kv_map, i
                                cudaStream_t s) {
   if (n_dec_grid > 0) {
     const int smem = decode_smem_bytes(D);
-    smem_attr_once(reinterpret_cast<const void*>(attn_decode_kernel<D, G>), smem);
-    dim3 grid(p.n_splits, p.hkv, n_dec_grid);
-    attn_decode_kernel<D, G><<<grid, 128, smem, s>>>(p);
+    if (p.sk_ctas > 0) {
+      smem_attr_once(reinterpret_cast<const void*>(attn_decode_sk_kernel<D, G>), smem);
+      attn_decode_sk_kernel<D, G><<<p.sk_ctas, 128, smem, s>>>(p);
+    } else {
+      smem_attr_once(reinterpret_cast<const void*>(attn_decode_kernel<D, G>), smem);
+      dim3 grid(p.n_splits, p.hkv, n_dec_grid);
+      attn_decode_kernel<D, G><<<grid, 128, smem, s>>>(p);
+    }
   }
   if (n_pt_grid > 0) launch_prefill_tc(p, kv_map, D, G, n_pt_grid, s);
+}
+
+// Resident CTAs of the stream-K decode kernel per SM (its grid = this x SMs).
+int decode_sk_ctas_per_sm(int head_dim, int group) {
+  int n = 0;
+  const int smem = decode_smem_bytes(head_dim);
+#define CS_SK_OCC(DD, GG)                                                                                 \
+  if (head_dim == DD && group == GG) {                                                                    \
+    smem_attr_once(reinterpret_cast<const void*>(attn_decode_sk_kernel<DD, GG>), smem);                   \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, attn_decode_sk_kernel<DD, GG>, 128, smem);          \
+  }
+  CS_SK_OCC(64, 1)
+  CS_SK_OCC(64, 2)
+  CS_SK_OCC(64, 4)
+  CS_SK_OCC(128, 1)
+  CS_SK_OCC(128, 2)
+  CS_SK_OCC(128, 4)
+  CS_SK_OCC(128, 5)
+  CS_SK_OCC(128, 8)
+#undef CS_SK_OCC
+  return n;
 }
 
 // Dispatch on (head_dim, group size); returns false for an unsupported shape.

@@ -106,6 +106,9 @@ struct AttnParams {
   float* ws2;                   // K2 split-K partials [tile][kvh][split] x {O [D][256], m [256], l [256]}
   int32_t layer, num_layers, hq, hkv, qkv_stride;
   int32_t n_splits, pages_per_split;   // K1: splits over pages
+  const int32_t* dec_pfx;       // [n_dec + 1] K1 stream-K: prefix sums of the decode entries' page counts
+  float* ws_sk;                 // K1 stream-K partials [cta][2] x {m[G], l[G], O[G][D]}
+  int32_t sk_ctas;              // K1 stream-K grid (0: the split-K kernel)
   int32_t k2_splits, k2_tiles_per_split;  // K2: splits over 128-key tiles
   float scale_log2;             // softmax_scale * log2(e)
 };

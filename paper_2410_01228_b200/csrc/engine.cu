@@ -64,6 +64,7 @@ void kv_move(bool to_host, __nv_bfloat16* pool, __nv_bfloat16* host_mapped, cons
 void kv_pack(bool to_stage, __nv_bfloat16* pool, __nv_bfloat16* stage, const void* segs, const int64_t* stage_off,
              int n_segs, int runs_per_seg, int D, int sms, cudaStream_t s);
 void fill_pool(__nv_bfloat16* pool, size_t n, uint64_t seed, cudaStream_t s);
+int decode_sk_ctas_per_sm(int head_dim, int group);
 bool launch_attention(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_dec_grid,
                       int n_pt_grid, cudaStream_t s);
 int prefill_tile_rows();
@@ -254,6 +255,8 @@ struct cs_engine {
   size_t ws_floats = 0;
   float* ws2 = nullptr;  // K2 split-K partials
   int32_t* dec_cnt = nullptr;  // K1 split-K arrival counters
+  float* ws_sk = nullptr;      // K1 stream-K partials
+  int sk_ctas = 0;             // K1 stream-K grid (0: split-K kernel)
   size_t ws2_floats = 0;
   uint8_t* d_meta = nullptr;
   uint8_t* h_meta = nullptr;
@@ -731,8 +734,16 @@ void cs_engine::tune_gemms(int M) {
     cublasLtMatmulPreferenceDestroy(pref);
     float best = 1e30f;
     int bi = -1;
+    // the lm_head runs replicated on every rank of a sharded engine: its
+    // algorithm must not depend on per-rank timing noise, or the ranks'
+    // logits (and sampled ids) could differ in the last bits
+    const bool replicated = sh.f32 && tp > 1;
     for (int i = 0; hs == CUBLAS_STATUS_SUCCESS && i < n; ++i) {
       if (res[i].state != CUBLAS_STATUS_SUCCESS) continue;
+      if (replicated) {
+        bi = i;
+        break;
+      }
       const float ms = time_over(sh, [&](const __nv_bfloat16* W) {
         return cublasLtMatmul(lt, pl.op, &alpha, W, pl.a, sh.A, pl.b, &beta, sh.C, pl.c, sh.C, pl.c, &res[i].algo,
                               blas_ws, wsz, s_compute) == CUBLAS_STATUS_SUCCESS;
@@ -752,7 +763,7 @@ void cs_engine::tune_gemms(int M) {
       cublasLtMatrixLayoutDestroy(pl.c);
     }
     // K7 against the best cuBLAS plan (CS_WGEMM=2)
-    if (wgemm_mode == 2 && csk::wgemm_supported(M, sh.N, sh.K)) {
+    if (wgemm_mode == 2 && !(sh.f32 && tp > 1) && csk::wgemm_supported(M, sh.N, sh.K)) {
       const float ms7 = time_over(sh, [&](const __nv_bfloat16* W) {
         return wgemm_launch(sh.A, W, sh.C, M, sh.N, sh.K, sh.f32);
       });
@@ -1195,7 +1206,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     const size_t o_desc = region(sizeof(csk::IterDesc));
     const size_t o_tok = region(sizeof(int32_t) * 3 * static_cast<size_t>(Tcap));
     const size_t o_ent = region(sizeof(int32_t) * 5 * E);
-    const size_t o_dec = region(sizeof(int32_t) * static_cast<size_t>(Dcap) + 4);
+    const size_t o_dec = region(sizeof(int32_t) * (2 * static_cast<size_t>(Dcap) + 1) + 4);  // dec_ent | dec_pfx
     const size_t o_tiles = region((sizeof(csk::PrefillTile) + 4) * tiles.size() + 8);
     const size_t o_bt = region(sizeof(int32_t) * bt.size() + 4);
     const size_t total = off;
@@ -1232,7 +1243,14 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     std::memcpy(he + 2 * E, ent_kvlen.data(), 4 * n);
     std::memcpy(he + 3 * E, ent_bt.data(), 4 * n);
     std::memcpy(he + 4 * E, ent_last.data(), 4 * n);
-    if (!dec_ent.empty()) std::memcpy(h + o_dec, dec_ent.data(), 4 * dec_ent.size());
+    if (!dec_ent.empty()) {
+      std::memcpy(h + o_dec, dec_ent.data(), 4 * dec_ent.size());
+      // K1 stream-K: page-count prefix over the decode entries (online first)
+      int32_t* pf = reinterpret_cast<int32_t*>(h + o_dec) + Dcap;
+      pf[0] = 0;
+      for (size_t k = 0; k < dec_ent.size(); ++k)
+        pf[k + 1] = pf[k] + (ent_kvlen[static_cast<size_t>(dec_ent[k])] + 15) / 16;
+    }
     if (!tiles.empty()) {
       // K2 launch order: heaviest tiles first (the block scheduler then runs a
       // longest-first list schedule over the SMs); ties keep plan order
@@ -1284,6 +1302,9 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     ap.ent_bt = ap.ent_q0 + 3 * E;
     ap.block_table = reinterpret_cast<const int32_t*>(d + o_bt);
     ap.dec_ent = reinterpret_cast<const int32_t*>(d + o_dec);
+    ap.dec_pfx = reinterpret_cast<const int32_t*>(d + o_dec) + Dcap;
+    ap.ws_sk = e->ws_sk;
+    ap.sk_ctas = e->sk_ctas;
     ap.tiles = reinterpret_cast<const csk::PrefillTile*>(d + o_tiles);
     ap.tile_order = reinterpret_cast<const int32_t*>(d + o_tiles + sizeof(csk::PrefillTile) * tiles.size());
     ap.ws = e->ws;
@@ -1522,6 +1543,16 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         CK(cudaMalloc(&e->d_out, sizeof(csk::IterDesc) + 8 * e->max_ent));
         CK(cudaMalloc(&e->dec_cnt, sizeof(int32_t) * e->max_ent * e->hkv));
         CK(cudaMemset(e->dec_cnt, 0, sizeof(int32_t) * e->max_ent * e->hkv));
+        {
+          // K1 stream-K: one resident wave over every SM (CS_K1_SPLITK=1: the
+          // per-(entry, head) split-K kernel instead, for A/B)
+          const char* sk = std::getenv("CS_K1_SPLITK");
+          if (!(sk && sk[0] == '1')) e->sk_ctas = csk::decode_sk_ctas_per_sm(e->D, e->G) * e->sms;
+          if (e->sk_ctas > 0) {
+            const size_t n = static_cast<size_t>(e->sk_ctas) * 2 * e->G * (e->D + 2);
+            CK(cudaMalloc(&e->ws_sk, n * 4));
+          }
+        }
         CK(cudaMallocHost(&e->h_out, sizeof(csk::IterDesc) + 8 * e->max_ent));
         CKB(cublasCreate(&e->blas));
         CKB(cublasSetStream(e->blas, e->s_compute));
@@ -1622,6 +1653,7 @@ int cs_destroy(cs_engine* e) {
                       static_cast<void*>(e->attn), static_cast<void*>(e->tmp), static_cast<void*>(e->gu),
                       static_cast<void*>(e->act), static_cast<void*>(e->xl), static_cast<void*>(e->logits),
                       static_cast<void*>(e->ws), static_cast<void*>(e->ws2), static_cast<void*>(e->dec_cnt),
+                      static_cast<void*>(e->ws_sk),
                       static_cast<void*>(e->d_meta),
                       static_cast<void*>(e->d_out),
                       e->blas_ws})

@@ -107,6 +107,33 @@ def test_k1_decode_and_k2_in_one_launch():
         eng.close()
 
 
+@pytest.mark.parametrize("ctx", [
+    [5, 1, 4000, 33, 2100, 16, 17, 900, 3999, 64] * 4,   # 40 rows: pairs cut by CTA ranges, CTAs over many pairs
+    [7999],                                             # one long row: 8 pairs spread over many CTAs
+])
+def test_k1_stream_k_mixed_lengths(ctx):
+    """K1 splits the flattened pages of all (entry, KV head) pairs into equal
+    ranges over one resident wave of CTAs; a pair cut by range boundaries is
+    folded from its covering CTAs' partials. Decode-only plan = the CUDA-graph
+    path; rows of 1..7999 context (partial pages, single-page pairs)."""
+    eng = _engine()
+    try:
+        for r, c in enumerate(ctx):
+            eng.register_request(r, r == 0)
+            done = 0
+            while done < c:  # write context KV with prefill chunks of <= 4000 tokens
+                n = min(4000, c - done)
+                _run(eng, [cs.BatchEntry(r, n, done, cs.CS_PREFILL, r == 0)], [n + (1 if done + n == c else 0)])
+                done += n
+        dec = [cs.BatchEntry(r, 1, c + 1, cs.CS_DECODE, r == 0) for r, c in enumerate(ctx)]
+        for rep in range(2):  # the second step replays the captured graph
+            _run(eng, dec, [1] * len(ctx))
+            _check_rows(eng, dec, [[c + rep] for c in ctx], len(ctx))
+            dec = [cs.BatchEntry(r, 1, c + 2, cs.CS_DECODE, r == 0) for r, c in enumerate(ctx)]
+    finally:
+        eng.close()
+
+
 def test_k2_lazy_rescale_path():
     """A key late in the sequence with a much larger score than everything
     before forces the O-in-TMEM correction (max grows by > 2^8 in log2 units)."""

@@ -23,6 +23,17 @@ if has decode; then
   timeout 600 $NCU --metrics gpu__time_duration.sum --csv --log-file "$OUT/decode_launches.csv" \
     python tools/decode_probe.py 39 4237 3 > "$OUT/decode_ncu.log" 2>&1
 fi
+if has k1ab; then
+  timeout 600 python -m pytest tests/test_gpu_attention.py -x -q > "$OUT/pytest_attention.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_attention.log"
+  for shape in "39 4237" "8 4237" "64 4224" "128 2000" "200 1000" "16 16000"; do
+    for mode in 0 1; do
+      CS_K1_SPLITK=$mode timeout 300 python tools/decode_probe.py $shape 8 >> "$OUT/k1ab.jsonl" 2>> "$OUT/k1ab.err"
+      echo "{\"mode_splitk\": $mode, \"shape\": \"$shape\"}" >> "$OUT/k1ab.jsonl"
+    done
+  done
+  timeout 600 $NCU --metrics gpu__time_duration.sum --csv --log-file "$OUT/decode_launches_sk.csv" \
+    python tools/decode_probe.py 39 4237 3 > "$OUT/decode_ncu_sk.log" 2>&1
+fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
@@ -40,7 +51,7 @@ if has k8; then
     python tools/ncu_targets.py gemm > "$OUT/k8.log" 2>&1
 fi
 if has k4; then
-  timeout 600 $NCU --set full --import-source on -k regex:kv_move -c 1 -o "$OUT/k4_gather" -f \
+  timeout 600 $NCU --set full --import-source on -k regex:"kv_pack|kv_move" -c 1 -o "$OUT/k4_gather" -f \
     python tools/ncu_targets.py gather > "$OUT/k4.log" 2>&1
 fi
 nvidia-smi -q -d CLOCK > "$OUT/clocks_end.txt" 2>&1
