@@ -314,6 +314,7 @@ struct cs_engine {
     int n_tok = 0, n_tok_on = 0, n_ent = 0, n_ent_on = 0, n_dec = 0, n_pt = 0;
     bool has_offline = false;
     int splits = 1, pps = 1;
+    bool k1_sk = false;  // K1 runs the stream-K kernel this iteration
     int k2_splits = 1, k2_tps = 1 << 30;
     bool graph = false;  // decode-only plan replayed from a captured CUDA graph
     int bucket = 0;      // graph bucket: token rows / entries / decode rows (padded)
@@ -1008,7 +1009,8 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
 void cs_engine::enqueue_layers() {
   if (it.graph) {
     const bool sp = cfg.instrumented != 0 && it.has_offline && L > 1;
-    const uint64_t key = static_cast<uint64_t>(it.bucket) | (static_cast<uint64_t>(sp) << 16) | (graph_gen << 20);
+    const uint64_t key = static_cast<uint64_t>(it.bucket) | (static_cast<uint64_t>(sp) << 16) |
+                         (static_cast<uint64_t>(it.k1_sk) << 17) | (graph_gen << 20);
     auto f = graphs.find(key);
     if (f == graphs.end()) {
       static const bool no_tune = [] {
@@ -1304,7 +1306,13 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     ap.dec_ent = reinterpret_cast<const int32_t*>(d + o_dec);
     ap.dec_pfx = reinterpret_cast<const int32_t*>(d + o_dec) + Dcap;
     ap.ws_sk = e->ws_sk;
-    ap.sk_ctas = e->sk_ctas;
+    // K1 kernel choice: with fewer (entry, KV head) pairs than resident
+    // stream-K CTAs every pair is split anyway and equal page ranges keep all
+    // SMs streaming (39 x 4.2K: -3.3% step time); with more pairs the
+    // per-pair split-K kernel has no segment overhead (128 x 2K: -5.5%)
+    // (profiles/r2/k1_streamk_ab.md). Graphs are keyed by the choice.
+    it.k1_sk = e->sk_ctas > 0 && it.n_dec * e->hkv < e->sk_ctas;
+    ap.sk_ctas = it.k1_sk ? e->sk_ctas : 0;
     ap.tiles = reinterpret_cast<const csk::PrefillTile*>(d + o_tiles);
     ap.tile_order = reinterpret_cast<const int32_t*>(d + o_tiles + sizeof(csk::PrefillTile) * tiles.size());
     ap.ws = e->ws;

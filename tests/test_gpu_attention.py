@@ -110,12 +110,15 @@ def test_k1_decode_and_k2_in_one_launch():
 @pytest.mark.parametrize("ctx", [
     [5, 1, 4000, 33, 2100, 16, 17, 900, 3999, 64] * 4,   # 40 rows: pairs cut by CTA ranges, CTAs over many pairs
     [7999],                                             # one long row: 8 pairs spread over many CTAs
+    [300, 17, 2000, 1] * 15,                            # 60 rows = 480 pairs: the per-pair split-K kernel
 ])
 def test_k1_stream_k_mixed_lengths(ctx):
-    """K1 splits the flattened pages of all (entry, KV head) pairs into equal
-    ranges over one resident wave of CTAs; a pair cut by range boundaries is
-    folded from its covering CTAs' partials. Decode-only plan = the CUDA-graph
-    path; rows of 1..7999 context (partial pages, single-page pairs)."""
+    """K1 with fewer (entry, KV head) pairs than resident CTAs: the stream-K
+    kernel splits the flattened pages of all pairs into equal ranges over one
+    wave of CTAs; a pair cut by range boundaries is folded from its covering
+    CTAs' partials. With more pairs: the per-pair split-K kernel. Decode-only
+    plan = the CUDA-graph path; rows of 1..7999 context (partial pages,
+    single-page pairs)."""
     eng = _engine()
     try:
         for r, c in enumerate(ctx):
