@@ -72,6 +72,8 @@ int prefill_tile_keys();
 int wgemm_stages(int Mp, size_t budget);
 int wgemm_max_clusters(int Mp, int stages, int splits);
 bool wgemm_supported(int M, int N, int K);
+void wgemm_sk(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, float* ws, int32_t* cnt, int M, int Mp,
+              int N, int K, bool f32_out, int ctas, cudaStream_t s);
 void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, int Mp, int N, int K, int splits,
               int stages, bool f32_out, cudaStream_t s);
 void p2p_allreduce(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s);
@@ -296,6 +298,9 @@ struct cs_engine {
   const CUtensorMap* tmap(const void* p, int rows, int K, int box_rows);
   bool wgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
   bool wgemm_launch(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
+  bool k7_sk = true;            // K7 in stream-K mode (CS_K7_SK=0: the cluster split-K kernel)
+  float* k7_ws = nullptr;       // stream-K partials
+  int32_t* k7_cnt = nullptr;    // stream-K per-tile arrival counters
   ncclComm_t comm = nullptr;
   DescRing ring[2];
   // K4/K5 DMA path: per-direction device staging (token-major, like a host
@@ -807,6 +812,11 @@ bool cs_engine::wgemm_launch(const __nv_bfloat16* A, const __nv_bfloat16* W, voi
   const CUtensorMap* wm = tmap(W, N, K, 128);
   const CUtensorMap* xm = tmap(A, M, K, Mp);
   if (!wm || !xm) return false;
+  if (k7_sk) {  // stream-K mode: one persistent CTA per SM, equal weight ranges
+    if (!k7_ws || N / 128 > 8192) return false;
+    csk::wgemm_sk(wm, xm, C, k7_ws, k7_cnt, M, Mp, N, K, out_f32, sms, s_compute);
+    return true;
+  }
   // ONE wave of CTAs: >= one feature tile per SM -> two CTAs per SM, no
   // split; fewer tiles -> one deep-ring CTA per SM and the largest K split
   // (a cluster of <= 8, any size, uneven last split) with n_tiles x split <=
@@ -1571,6 +1581,8 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         {
           // K7 for the M <= 256 projections: 2 (default) where start-up
           // tuning timed it faster than the best cuBLAS plan, 1 always, 0 never
+          const char* ksk = std::getenv("CS_K7_SK");
+          e->k7_sk = !(ksk && ksk[0] == '0');
           const char* v = std::getenv("CS_WGEMM");
           e->wgemm_mode = (v && v[0] == '1') ? 1 : (v && v[0] == '0') ? 0 : 2;
         }
@@ -1582,6 +1594,12 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         //   K2 splits: tiles*hkv*splits < 2 * sms whenever splits > 1
         e->ws_floats = static_cast<size_t>(2 * 4 * e->sms) * e->G * (2 + e->D);
         CK(cudaMalloc(&e->ws, e->ws_floats * 4));
+        //   K7 stream-K: [SM][2 slots][Mp <= 256][128 features] fp32 + per-tile counters
+        if (e->k7_sk) {
+          CK(cudaMalloc(&e->k7_ws, static_cast<size_t>(e->sms) * 2 * 256 * 128 * 4));
+          CK(cudaMalloc(&e->k7_cnt, sizeof(int32_t) * 8192));
+          CK(cudaMemset(e->k7_cnt, 0, sizeof(int32_t) * 8192));
+        }
         e->ws2_floats = static_cast<size_t>(2 * e->sms) * (e->D + 2) * 256;
         CK(cudaMalloc(&e->ws2, e->ws2_floats * 4));
         const size_t E = static_cast<size_t>(e->max_ent);
@@ -1661,7 +1679,7 @@ int cs_destroy(cs_engine* e) {
                       static_cast<void*>(e->attn), static_cast<void*>(e->tmp), static_cast<void*>(e->gu),
                       static_cast<void*>(e->act), static_cast<void*>(e->xl), static_cast<void*>(e->logits),
                       static_cast<void*>(e->ws), static_cast<void*>(e->ws2), static_cast<void*>(e->dec_cnt),
-                      static_cast<void*>(e->ws_sk),
+                      static_cast<void*>(e->ws_sk), static_cast<void*>(e->k7_ws), static_cast<void*>(e->k7_cnt),
                       static_cast<void*>(e->d_meta),
                       static_cast<void*>(e->d_out),
                       e->blas_ws})

@@ -208,6 +208,243 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 1) tc::tmem_dealloc<256>(tmem);
 }
 
+// ------------------------------------------------------ K7 stream-K mode --
+// Same swap-AB operands as above, but ONE persistent CTA per SM walks an
+// equal contiguous range of the flattened (feature tile, 64-wide K chunk)
+// units, so every SM streams the same number of weight bytes whatever N / 128
+// is (gate|up 224 tiles, qkv 48, o/down 32 on 148 SMs), and the TMA ring runs
+// on across tile boundaries. The accumulator is double-buffered in TMEM:
+// the epilogue of one tile segment overlaps the next segment's main loop. A
+// tile cut by range boundaries leaves an fp32 partial per covering CTA in a
+// global workspace (slot 0 = the CTA's first segment, slot 1 = its last);
+// the last covering CTA to finish (per-tile counter, self-resetting) folds
+// them. Roles (192 threads): warp 0 TMA, warp 1 UMMA issuer + TMEM owner,
+// warps 2-5 epilogue (warp w drains TMEM lanes 32 (w % 4) .. +31 = features).
+struct WskArgs {
+  void* y;
+  float* ws;        // [gridDim.x][2][Mp][128] fp32 partials
+  int32_t* cnt;     // [N / 128] arrival counters (zero between launches)
+  int32_t M, Mp, N, K;
+  int32_t f32_out;
+  int32_t stages;
+};
+
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__global__ void __launch_bounds__(192, 1)
+    wgemm_sk_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap xmap, WskArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int Mp = a.Mp;
+  const uint32_t stage_bytes = kWBytes + static_cast<uint32_t>(Mp) * 128;
+  const int S = a.stages;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+  uint64_t* full = bars;                       // [S]
+  uint64_t* empty = bars + kMaxStages;         // [S]
+  uint64_t* acc_full = bars + 2 * kMaxStages;  // [2]
+  uint64_t* acc_empty = acc_full + 2;          // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  int* s_last = reinterpret_cast<int*>(tslot + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int C = a.K / kKc;          // K chunks per tile
+  const int U = (a.N / kFeat) * C;  // units
+  const int W = (U + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
+  const int u0 = static_cast<int>(blockIdx.x) * W;
+  const int u1 = min(U, u0 + W);
+  const int n = max(0, u1 - u0);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&acc_full[i], 1);
+      tc::mbar_init(&acc_empty[i], 128);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&wmap);
+    tc::prefetch_tmap(&xmap);
+  }
+  if (warp == 1) {
+    if (Mp <= 64) tc::tmem_alloc<128>(tslot);
+    else if (Mp <= 128) tc::tmem_alloc<256>(tslot);
+    else tc::tmem_alloc<512>(tslot);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer --
+    // weights first (independent of the previous kernel: before the PDL wait)
+    const int pre = min(S, n);
+    if (tc::elect_one_sync()) {
+      for (int i = 0; i < pre; ++i) {
+        const int u = u0 + i;
+        tc::mbar_expect_tx(&full[i], stage_bytes);
+        tc::tma_load_2d(smem + i * stage_bytes, &wmap, &full[i], (u % C) * kKc, (u / C) * kFeat);
+      }
+    }
+    __syncwarp();
+    pdl_wait();
+    for (int i = 0; i < n; ++i) {
+      const int st = i % S;
+      const int u = u0 + i;
+      if (i >= S) tc::mbar_wait(&empty[st], ((i / S) - 1) & 1);
+      if (tc::elect_one_sync()) {
+        uint8_t* sw = smem + st * stage_bytes;
+        if (i >= pre) {
+          tc::mbar_expect_tx(&full[st], stage_bytes);
+          tc::tma_load_2d(sw, &wmap, &full[st], (u % C) * kKc, (u / C) * kFeat);
+        }
+        tc::tma_load_2d(sw + kWBytes, &xmap, &full[st], (u % C) * kKc, 0);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer --
+    const uint32_t idesc = tc::idesc_bf16_f32(kFeat, Mp, false, false);
+    const uint32_t base = tc::smem_u32(smem);
+    int seg = 0;
+    for (int i = 0; i < n; ++i) {
+      const int st = i % S;
+      const int u = u0 + i;
+      const bool first = i == 0 || u % C == 0;
+      const bool last = i == n - 1 || u % C == C - 1;
+      const int b = seg & 1;
+      if (first && seg >= 2) tc::mbar_wait(&acc_empty[b], ((seg >> 1) - 1) & 1);
+      tc::mbar_wait(&full[st], (i / S) & 1);
+      tc::tc_fence_after();
+      if (tc::elect_one_sync()) {
+        const uint32_t wa = base + st * stage_bytes, xa = wa + kWBytes;
+        const uint32_t d = tmem + static_cast<uint32_t>(b * Mp);
+#pragma unroll
+        for (int ks = 0; ks < kKc / 16; ++ks)
+          tc::umma_bf16_ss(d, tc::sdesc_sw128(wa + ks * 32, 16, 1024), tc::sdesc_sw128(xa + ks * 32, 16, 1024),
+                           idesc, (!first || ks > 0) ? 1u : 0u);
+        tc::umma_commit(&empty[st]);
+        if (last) tc::umma_commit(&acc_full[b]);
+      }
+      __syncwarp();
+      if (last) ++seg;
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue --
+    const int f = (warp & 3) * 32 + lane;  // feature row of the tile = TMEM lane
+    const uint32_t tl = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    int seg = 0;
+    int u = u0;
+    while (u < u1) {
+      const int t = u / C;
+      const int c_lo = u % C;
+      const int seg_end = min(u1, (t + 1) * C);
+      const bool full_tile = c_lo == 0 && seg_end == (t + 1) * C;
+      const bool first_seg = u == u0;
+      u = seg_end;
+      const int b = seg & 1;
+      tc::mbar_wait(&acc_full[b], (seg >> 1) & 1);
+      tc::tc_fence_after();
+      const int n0 = t * kFeat;
+      float* part = a.ws + ((static_cast<size_t>(blockIdx.x) * 2 + (first_seg ? 0 : 1)) * Mp) * kFeat;
+      for (int c0 = 0; c0 < Mp; c0 += 32) {
+        float v[32];
+        tc::tmem_ld32(tl + static_cast<uint32_t>(b * Mp + c0), v);
+        tc::tmem_wait_ld();
+        tc::reg_fence<32>(v);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int tok = c0 + k;
+          if (tok >= a.M) break;
+          if (full_tile) {
+            const size_t o = static_cast<size_t>(tok) * a.N + n0 + f;
+            if (a.f32_out) static_cast<float*>(a.y)[o] = v[k];
+            else static_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16(v[k]);
+          } else {
+            __stcg(part + static_cast<size_t>(tok) * kFeat + f, v[k]);
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&acc_empty[b]);
+      ++seg;
+      if (!full_tile) {
+        // the last CTA covering tile t folds its partials
+        const int c_first = (t * C) / W, c_last = ((t + 1) * C - 1) / W;
+        __threadfence();
+        epi_bar_sync();
+        if (threadIdx.x == 64) *s_last = atomicAdd(a.cnt + t, 1) == c_last - c_first;
+        epi_bar_sync();
+        if (*s_last) {
+          __threadfence();
+          for (int tok = 0; tok < a.M; ++tok) {
+            float acc = 0.f;
+            for (int cc = c_first; cc <= c_last; ++cc) {
+              const int slot = cc * W >= t * C ? 0 : 1;
+              acc += __ldcg(a.ws + ((static_cast<size_t>(cc) * 2 + slot) * Mp + tok) * kFeat + f);
+            }
+            const size_t o = static_cast<size_t>(tok) * a.N + n0 + f;
+            if (a.f32_out) static_cast<float*>(a.y)[o] = acc;
+            else static_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16(acc);
+          }
+          if (threadIdx.x == 64) a.cnt[t] = 0;
+        }
+        epi_bar_sync();  // s_last is rewritten by the next cut tile
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 1) {
+    if (Mp <= 64) tc::tmem_dealloc<128>(tmem);
+    else if (Mp <= 128) tc::tmem_dealloc<256>(tmem);
+    else tc::tmem_dealloc<512>(tmem);
+  }
+}
+
+size_t wgemm_sk_smem_bytes(int Mp, int stages) {
+  return static_cast<size_t>(stages) * (kWBytes + static_cast<size_t>(Mp) * 128) + 256 + 1024;
+}
+
+int wgemm_sk_stages(int Mp) {
+  int s = kMaxStages;
+  while (s > 2 && wgemm_sk_smem_bytes(Mp, s) > 220 * 1024) --s;
+  return s;
+}
+
+// Stream-K launch: grid = `ctas` (<= SMs, one resident CTA each), ws >= ctas x
+// 2 x Mp x 128 floats, cnt >= N / 128 zeroed ints.
+void wgemm_sk(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, float* ws, int32_t* cnt, int M, int Mp,
+              int N, int K, bool f32_out, int ctas, cudaStream_t s) {
+  smem_attr_once(reinterpret_cast<const void*>(wgemm_sk_kernel), 227 * 1024);
+  WskArgs a{};
+  a.y = y;
+  a.ws = ws;
+  a.cnt = cnt;
+  a.M = M;
+  a.Mp = Mp;
+  a.N = N;
+  a.K = K;
+  a.f32_out = f32_out ? 1 : 0;
+  a.stages = wgemm_sk_stages(Mp);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas, 1, 1);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = wgemm_sk_smem_bytes(Mp, a.stages);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: weights stream during the producer's tail
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, wgemm_sk_kernel, *wmap, *xmap, a);
+}
+
 size_t wgemm_smem_bytes(int Mp, int stages) {
   const size_t stage = kWBytes + static_cast<size_t>(Mp) * 128;
   const size_t ring = stages * stage, red = static_cast<size_t>(Mp) * kFeat * 4;

@@ -22,15 +22,26 @@ def _bench(eng, M, N, K):
     return d.value, r.value
 
 
-@pytest.fixture(scope="module")
-def eng():
-    e = cs.Engine(cs.model_config("tiny", gpu_kv_capacity=1 << 26))
+@pytest.fixture(scope="module", params=["stream-k", "cluster"])
+def eng(request):
+    """K7 in its default stream-K mode (one persistent CTA per SM over equal
+    (tile, K-chunk) ranges, cut tiles folded from fp32 partials) and in the
+    cluster split-K mode (CS_K7_SK=0: DSMEM reduction)."""
+    old = os.environ.get("CS_K7_SK")
+    os.environ["CS_K7_SK"] = "1" if request.param == "stream-k" else "0"
+    try:
+        e = cs.Engine(cs.model_config("tiny", gpu_kv_capacity=1 << 26))
+    finally:
+        if old is None:
+            os.environ.pop("CS_K7_SK")
+        else:
+            os.environ["CS_K7_SK"] = old
     yield e
     e.close()
 
 
 @pytest.mark.parametrize("M", [1, 8, 17, 64, 128, 200, 256])
-@pytest.mark.parametrize("N,K", [(6144, 4096), (4096, 14336), (128, 64), (28672, 4096), (512, 256)])
+@pytest.mark.parametrize("N,K", [(6144, 4096), (4096, 14336), (128, 64), (28672, 4096), (512, 256), (128256, 4096)])
 def test_k7_matches_cublas(eng, M, N, K):
     diff, ref = _bench(eng, M, N, K)
     assert ref > 0

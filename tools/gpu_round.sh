@@ -34,6 +34,17 @@ if has k1ab; then
   timeout 600 $NCU --metrics gpu__time_duration.sum --csv --log-file "$OUT/decode_launches_sk.csv" \
     python tools/decode_probe.py 39 4237 3 > "$OUT/decode_ncu_sk.log" 2>&1
 fi
+if has gemmab; then
+  timeout 900 python -m pytest tests/test_gpu_wgemm.py -x -q > "$OUT/pytest_wgemm.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_wgemm.log"
+  CS_K7_SK=1 timeout 600 python tools/gemm_k7.py 50 > "$OUT/gemm_sk.jsonl" 2> "$OUT/gemm_sk.err"
+  CS_K7_SK=0 timeout 600 python tools/gemm_k7.py 50 > "$OUT/gemm_cluster.jsonl" 2> "$OUT/gemm_cluster.err"
+  for w in 2 1 0; do
+    CS_WGEMM=$w timeout 300 python tools/decode_probe.py 39 4237 8 >> "$OUT/decode_wgemm.jsonl" 2>> "$OUT/decode_wgemm.err"
+    echo "{\"wgemm\": $w}" >> "$OUT/decode_wgemm.jsonl"
+  done
+  CS_WGEMM=1 timeout 600 $NCU --metrics gpu__time_duration.sum --csv --log-file "$OUT/decode_launches_k7.csv" \
+    python tools/decode_probe.py 39 4237 3 > "$OUT/decode_ncu_k7.log" 2>&1
+fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
