@@ -298,7 +298,7 @@ struct cs_engine {
   const CUtensorMap* tmap(const void* p, int rows, int K, int box_rows);
   bool wgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
   bool wgemm_launch(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
-  bool k7_sk = true;            // K7 in stream-K mode (CS_K7_SK=0: the cluster split-K kernel)
+  bool k7_sk = false;           // K7 in stream-K mode (CS_K7_SK=1; default: the cluster split-K kernel)
   float* k7_ws = nullptr;       // stream-K partials
   int32_t* k7_cnt = nullptr;    // stream-K per-tile arrival counters
   ncclComm_t comm = nullptr;
@@ -1582,7 +1582,7 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
           // K7 for the M <= 256 projections: 2 (default) where start-up
           // tuning timed it faster than the best cuBLAS plan, 1 always, 0 never
           const char* ksk = std::getenv("CS_K7_SK");
-          e->k7_sk = !(ksk && ksk[0] == '0');
+          e->k7_sk = ksk && ksk[0] == '1';
           const char* v = std::getenv("CS_WGEMM");
           e->wgemm_mode = (v && v[0] == '1') ? 1 : (v && v[0] == '0') ? 0 : 2;
         }

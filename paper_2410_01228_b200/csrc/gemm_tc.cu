@@ -381,15 +381,28 @@ __global__ void __launch_bounds__(192, 1)
         epi_bar_sync();
         if (*s_last) {
           __threadfence();
-          for (int tok = 0; tok < a.M; ++tok) {
-            float acc = 0.f;
+          // 16 tokens per pass: the partial loads of a pass are independent
+          // (in flight together) instead of one L2 round trip per token
+          for (int t0 = 0; t0 < a.M; t0 += 16) {
+            float acc[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) acc[k] = 0.f;
             for (int cc = c_first; cc <= c_last; ++cc) {
               const int slot = cc * W >= t * C ? 0 : 1;
-              acc += __ldcg(a.ws + ((static_cast<size_t>(cc) * 2 + slot) * Mp + tok) * kFeat + f);
+              const float* pp = a.ws + ((static_cast<size_t>(cc) * 2 + slot) * Mp + t0) * kFeat + f;
+              float v[16];
+#pragma unroll
+              for (int k = 0; k < 16; ++k) v[k] = t0 + k < Mp ? __ldcg(pp + k * kFeat) : 0.f;
+#pragma unroll
+              for (int k = 0; k < 16; ++k) acc[k] += v[k];
             }
-            const size_t o = static_cast<size_t>(tok) * a.N + n0 + f;
-            if (a.f32_out) static_cast<float*>(a.y)[o] = acc;
-            else static_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16(acc);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              if (t0 + k >= a.M) break;
+              const size_t o = static_cast<size_t>(t0 + k) * a.N + n0 + f;
+              if (a.f32_out) static_cast<float*>(a.y)[o] = acc[k];
+              else static_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16(acc[k]);
+            }
           }
           if (threadIdx.x == 64) a.cnt[t] = 0;
         }
