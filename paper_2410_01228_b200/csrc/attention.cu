@@ -524,6 +524,8 @@ int decode_smem_bytes(int D) { return 4 * 4 * kPage * D * 2 > (4 * 16 * 2 + 4 * 
 
 bool launch_prefill_tc(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_pt_grid,
                        cudaStream_t s);
+bool launch_prefill_tc2(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_pt_grid,
+                        cudaStream_t s);
 
 template <int D, int G>
 static void launch_attention_t(const AttnParams& p, const CUtensorMap* kv_map, int n_dec_grid, int n_pt_grid,
@@ -539,7 +541,9 @@ static void launch_attention_t(const AttnParams& p, const CUtensorMap* kv_map, i
       attn_decode_kernel<D, G><<<grid, 128, smem, s>>>(p);
     }
   }
-  if (n_pt_grid > 0) launch_prefill_tc(p, kv_map, D, G, n_pt_grid, s);
+  if (n_pt_grid > 0) {
+    if (!(p.k2_pair && launch_prefill_tc2(p, kv_map, D, G, n_pt_grid, s))) launch_prefill_tc(p, kv_map, D, G, n_pt_grid, s);
+  }
 }
 
 // Resident CTAs of the stream-K decode kernel per SM (its grid = this x SMs).

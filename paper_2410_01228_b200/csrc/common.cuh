@@ -110,6 +110,7 @@ struct AttnParams {
   float* ws_sk;                 // K1 stream-K partials [cta][2] x {m[G], l[G], O[G][D]}
   int32_t sk_ctas;              // K1 stream-K grid (0: the split-K kernel)
   int32_t k2_splits, k2_tiles_per_split;  // K2: splits over 128-key tiles
+  int32_t k2_pair;                        // K2 on CTA pairs (attn_tc2.cu, head_dim 128)
   float scale_log2;             // softmax_scale * log2(e)
 };
 

@@ -68,6 +68,7 @@ int decode_sk_ctas_per_sm(int head_dim, int group);
 bool launch_attention(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_dec_grid,
                       int n_pt_grid, cudaStream_t s);
 int prefill_tile_rows();
+int prefill_tc2_tile_rows();
 int prefill_tile_keys();
 int wgemm_stages(int Mp, size_t budget);
 int wgemm_max_clusters(int Mp, int stages, int splits);
@@ -259,6 +260,7 @@ struct cs_engine {
   int32_t* dec_cnt = nullptr;  // K1 split-K arrival counters
   float* ws_sk = nullptr;      // K1 stream-K partials
   int sk_ctas = 0;             // K1 stream-K grid (0: split-K kernel)
+  bool k2_pair = false;        // K2 on CTA pairs (head_dim 128; CS_K2_1CTA=1: the single-CTA kernel)
   size_t ws2_floats = 0;
   uint8_t* d_meta = nullptr;
   uint8_t* h_meta = nullptr;
@@ -1125,7 +1127,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
         // K2 work tiles: prefill_tile_rows() packed (token, head-in-group) rows
         const int rows = static_cast<int>(pos.size()) * e->G;
         max_pre_kv = std::max(max_pre_kv, kv_len);
-        const int step = csk::prefill_tile_rows();
+        const int step = e->k2_pair ? csk::prefill_tc2_tile_rows() : csk::prefill_tile_rows();
         for (int r0 = 0; r0 < rows; r0 += step) {
           tiles.push_back({i, r0});
           const int last = std::min(r0 + step, rows) - 1;
@@ -1280,7 +1282,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     it.k2_splits = 1;
     it.k2_tps = 1 << 30;
     if (it.n_pt > 0) {
-      const int ctas = it.n_pt * e->hkv;
+      const int ctas = it.n_pt * e->hkv * (e->k2_pair ? 2 : 1);  // SMs per unit: a CTA pair or one CTA
       const int kt = csk::prefill_tile_keys();
       const int max_kt = (max_pre_kv + kt - 1) / kt;
       if (ctas < e->sms && max_kt >= 8) {
@@ -1288,7 +1290,8 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
         if (S2 > 1) {
           it.k2_tps = (max_kt + S2 - 1) / S2;
           it.k2_splits = (max_kt + it.k2_tps - 1) / it.k2_tps;
-          const size_t need = static_cast<size_t>(it.n_pt) * e->hkv * it.k2_splits * (e->D + 2) * 256;
+          const size_t need = static_cast<size_t>(it.n_pt) * e->hkv * it.k2_splits * (e->D + 2) *
+                              (e->k2_pair ? csk::prefill_tc2_tile_rows() : csk::prefill_tile_rows());
           if (need > e->ws2_floats) {
             if (e->ws2) CK(cudaFree(e->ws2));
             e->ws2_floats = need * 2;
@@ -1334,6 +1337,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     ap.n_splits = it.splits;
     ap.ws2 = e->ws2;
     ap.k2_splits = it.k2_splits;
+    ap.k2_pair = e->k2_pair ? 1 : 0;
     ap.k2_tiles_per_split = it.k2_tps;
     ap.pages_per_split = it.pps;
     ap.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(e->D));
@@ -1564,6 +1568,8 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         {
           // K1 stream-K: one resident wave over every SM (CS_K1_SPLITK=1: the
           // per-(entry, head) split-K kernel instead, for A/B)
+          const char* k2s = std::getenv("CS_K2_1CTA");
+          e->k2_pair = e->D == 128 && !(k2s && k2s[0] == '1');
           const char* sk = std::getenv("CS_K1_SPLITK");
           if (!(sk && sk[0] == '1')) e->sk_ctas = csk::decode_sk_ctas_per_sm(e->D, e->G) * e->sms;
           if (e->sk_ctas > 0) {
