@@ -260,7 +260,7 @@ struct cs_engine {
   int32_t* dec_cnt = nullptr;  // K1 split-K arrival counters
   float* ws_sk = nullptr;      // K1 stream-K partials
   int sk_ctas = 0;             // K1 stream-K grid (0: split-K kernel)
-  bool k2_pair = false;        // K2 on CTA pairs (head_dim 128; CS_K2_1CTA=1: the single-CTA kernel)
+  bool k2_pair = false;        // K2 on CTA pairs (head_dim 128; opt-in CS_K2_PAIR=1)
   size_t ws2_floats = 0;
   uint8_t* d_meta = nullptr;
   uint8_t* h_meta = nullptr;
@@ -1568,8 +1568,10 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         {
           // K1 stream-K: one resident wave over every SM (CS_K1_SPLITK=1: the
           // per-(entry, head) split-K kernel instead, for A/B)
-          const char* k2s = std::getenv("CS_K2_1CTA");
-          e->k2_pair = e->D == 128 && !(k2s && k2s[0] == '1');
+          // K2 on CTA pairs measured slower than the single-CTA kernel
+          // (profiles/r2/k2_pair_ab.md): opt-in only (CS_K2_PAIR=1)
+          const char* k2s = std::getenv("CS_K2_PAIR");
+          e->k2_pair = e->D == 128 && k2s && k2s[0] == '1';
           const char* sk = std::getenv("CS_K1_SPLITK");
           if (!(sk && sk[0] == '1')) e->sk_ctas = csk::decode_sk_ctas_per_sm(e->D, e->G) * e->sms;
           if (e->sk_ctas > 0) {

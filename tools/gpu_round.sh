@@ -47,8 +47,9 @@ if has gemmab; then
 fi
 if has k2ab; then
   timeout 600 python -m pytest tests/test_gpu_attention.py -x -q > "$OUT/pytest_attention.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_attention.log"
-  CS_K2_1CTA=1 timeout 600 python tools/k2_sweep.py 20 > "$OUT/k2_1cta.jsonl" 2> "$OUT/k2_1cta.err"
-  timeout 600 python tools/k2_sweep.py 20 > "$OUT/k2_pair.jsonl" 2> "$OUT/k2_pair.err"
+  timeout 600 python tools/k2_sweep.py 20 > "$OUT/k2_1cta.jsonl" 2> "$OUT/k2_1cta.err"
+  CS_K2_PAIR=1 timeout 600 python tools/k2_sweep.py 20 > "$OUT/k2_pair.jsonl" 2> "$OUT/k2_pair.err"
+  CS_K2_PAIR=1 timeout 600 python -m pytest tests/test_gpu_attention.py -x -q > "$OUT/pytest_attention_pair.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_attention_pair.log"
 fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
