@@ -85,11 +85,19 @@ SHAPES = {  # SURVEY.md 8 model table (public HF configs)
 
 
 def peaks():
+    """(HBM GB/s, bf16 TFLOP/s burst, bf16 TFLOP/s sustained, provenance). The
+    burst figure is the roofline of a kernel timed alone (the fixed-shape
+    probes); the sustained one (back-to-back GEMMs for 4 s, under the power
+    cap) of a kernel timed inside the long co-serving run (the window's
+    kernel classes)."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured (MEASURED_PEAKS.json, burst)"
-    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+        burst = d.get("bf16_tflops", 1590.0)
+        return (d.get("hbm_gbs", 6650.0), burst, d.get("bf16_tflops_sustained", burst),
+                "measured (MEASURED_PEAKS.json): bf16 sustained for the in-window kernel classes, burst for the "
+                "fixed-shape probes; HBM copy peak for both")
+    return 6650.0, 1590.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
 def percentile(xs, q):
@@ -531,7 +539,7 @@ def main():
     import paper_2410_01228_b200 as cs
     from paper_2410_01228_b200 import _ffi as F
     from paper_2410_01228_b200 import replay as R
-    hbm_peak, bf16_peak, peak_kind = peaks()
+    hbm_peak, bf16_peak, bf16_sus, peak_kind = peaks()
     tp = world > 1 and not args.replicas
     mode = mode_of(world, args.replicas)
 
@@ -679,9 +687,9 @@ def main():
     kinfo = {}
     for cls, key, bound, unit, scale, peak, tkey in (
             (F.CS_KT_K8, "K8 gemm_pf_kernel (layer projections, tcgen05 cta_group::2)", "tensor", "TFLOP/s", 1e12,
-             bf16_peak, "K8"),
+             bf16_sus, "K8"),
             (F.CS_KT_K2, "K2 attn_prefill_tc_kernel (prefill paged attention, tcgen05)", "tensor", "TFLOP/s", 1e12,
-             bf16_peak, "K2"),
+             bf16_sus, "K2"),
             (F.CS_KT_K1, "K1 attn_decode_kernel (decode paged attention)", "hbm", "GB/s", 1e9, hbm_peak, "K1")):
         t = rp["kt"][cls]
         if t.launches == 0 or t.ms <= 0:
