@@ -598,6 +598,7 @@ def main():
             assert p.mismatches == 0, f"replay diverged from the reference at op {p.first_mismatch_op}"
         cat = lambda f: np.concatenate([getattr(p, f) for p in parts])
         wall_ms = np.array([p.wall_ms for p in parts])
+        op_ms = np.sum([p.op_ms for p in parts], axis=0)
         # per-iteration wall clock of the whole window (each step restarts its clock)
         t_end = np.concatenate([p.wall_end_ms + (wall_ms[:i].sum()) for i, p in enumerate(parts)])
         it0, it1 = sl[0][0], sl[-1][1]
@@ -623,7 +624,7 @@ def main():
                     clocks=clocks, setup_s=setup_s, kt=kt, gpu_ms=gpu_ms, step_ms=step_ms,
                     dropped=cat("dropped_layer"), drop_us=cat("drop_latency_us"), pre_drop=cat("pre_drop_layer_us"),
                     h2d=cat("h2d_bytes"), d2h=cat("d2h_bytes"), iters=int(sum(p.iterations for p in parts)),
-                    ranks_ckpt=ranks_ckpt)
+                    ranks_ckpt=ranks_ckpt, op_ms=op_ms)
 
     rp = replay(args.workload)
     reps = world if (world > 1 and not tp) else 1
@@ -752,7 +753,10 @@ def main():
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": float(rp["h2d"].sum()) / K,
                 "d2h_bytes_per_step": float(rp["d2h"].sum()) / K,
                 "what": "offline tokens / wall time of the replay through the C-ABI (host plan buffers: H2D plan "
-                        "metadata, D2H sampled ids, every iteration)"},
+                        "metadata, D2H sampled ids, every iteration)",
+                "wall_s": wall_s, "device_s": gpu_s,
+                "host_ms_by_op": {k: round(float(rp["op_ms"][c]), 1) for k, c in R.OPC.items()
+                                  if float(rp["op_ms"][c]) >= 0.05}},
         "online_p99_tpot_ms": percentile(tpot, 0.99), "online_p99_tbt_ms": percentile(tbt, 0.99),
         "slo_tbt_ms": slo_tbt, "slo_met": bool(percentile(tbt, 0.99) <= slo_tbt),
         "offline_tokens": off, "online_tokens": on, "iterations": rp["iters"],

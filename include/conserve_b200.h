@@ -303,6 +303,9 @@ int cs_kernel_timing(cs_engine* e, int32_t cls, cs_ktime* out);
 typedef struct {
   int64_t iterations, mismatches, first_mismatch_op;
   double wall_ms;
+  /* host wall ms spent in each replayed op kind (index = op code: 14 dispatch
+   * = plan build + enqueue, 16 iteration end = blocked on the device + outputs) */
+  double op_ms[20];
 } cs_replay_stats;
 int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin, int64_t op_end, const int64_t* plans,
                   double* gpu_ms, double* wall_end_ms, int32_t* dropped_layer, double* drop_latency_us,

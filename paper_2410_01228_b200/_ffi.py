@@ -110,7 +110,7 @@ class cs_iter_info(C.Structure):
 
 class cs_replay_stats(C.Structure):
     _fields_ = [("iterations", C.c_int64), ("mismatches", C.c_int64), ("first_mismatch_op", C.c_int64),
-                ("wall_ms", C.c_double)]
+                ("wall_ms", C.c_double), ("op_ms", C.c_double * 20)]
 
 
 # (name, argtypes) for every export declared in include/conserve_b200.h

@@ -74,6 +74,7 @@ extern "C" int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin,
   for (int64_t i = op_begin; i < op_end; ++i) {
     const int64_t* o = ops + 8 * i;
     int rc = CS_OK;
+    const double t_op = now_ms();
     switch (o[0]) {
       case kRegister:
         rc = cs_kv_register_request(e, o[1], static_cast<int32_t>(o[2]));
@@ -210,6 +211,7 @@ extern "C" int cs_replay_run(cs_engine* e, const int64_t* ops, int64_t op_begin,
       default:
         rc = CS_ERR_INVALID;
     }
+    if (o[0] >= 0 && o[0] < 20) st->op_ms[o[0]] += now_ms() - t_op;
     if (rc != CS_OK) {
       st->iterations = it;
       st->wall_ms = now_ms() - t0;

@@ -140,6 +140,7 @@ class WindowResult:
     mismatches: int
     first_mismatch_op: int
     wall_ms: float
+    op_ms: np.ndarray  # host ms per replayed op kind (OPC codes)
     gpu_ms: np.ndarray
     wall_end_ms: np.ndarray
     dropped_layer: np.ndarray
@@ -175,7 +176,7 @@ def run(eng: Engine, tr: Trace, it_begin: int, it_end: int, dry: bool = False,
         raise RuntimeError(f"replay failed at op {st.first_mismatch_op} "
                            f"({tr.ops[st.first_mismatch_op].tolist()}): rc={rc} {msg}")
     _check(lib().cs_set_dry(eng._h, 0))
-    return WindowResult(st.iterations, st.mismatches, st.first_mismatch_op, st.wall_ms, **arrs)
+    return WindowResult(st.iterations, st.mismatches, st.first_mismatch_op, st.wall_ms, np.array(st.op_ms[:]), **arrs)
 
 
 def engine_config_for(tr: Trace, preset: str, **overrides) -> F.cs_config:

@@ -59,6 +59,10 @@ if has k1; then
   timeout 600 $NCU --set full --import-source on -k regex:attn_decode_kernel -s 1 -c 1 -o "$OUT/k1_decode" -f \
     python tools/ncu_targets.py decode > "$OUT/k1.log" 2>&1
 fi
+if has k1sk; then
+  timeout 600 $NCU --set full --import-source on -k regex:attn_decode -s 1 -c 1 -o "$OUT/k1sk_decode" -f \
+    python tools/ncu_targets.py decode 3 39 4237 > "$OUT/k1sk.log" 2>&1
+fi
 if has k2; then
   timeout 600 $NCU --set full --import-source on -k regex:attn_prefill -s 1 -c 1 -o "$OUT/k2_prefill" -f \
     python tools/ncu_targets.py prefill > "$OUT/k2.log" 2>&1
