@@ -211,6 +211,21 @@ int32_t BlockPool::block_for_read(int64_t id, size_t page_idx) {
   throw LogicError("attention reads a page whose block was reallocated");
 }
 
+void BlockPool::blocks_for_read(int64_t id, size_t n, std::vector<int32_t>& out, int64_t& wait_h2d) {
+  Req& r = req(id);
+  for (size_t pg = 0; pg < n; ++pg) {
+    int32_t b;
+    if (pg < r.pages.size()) {
+      const Page& p = r.pages[pg];
+      b = (p.on_gpu && !p.discarded && p.block >= 0) ? p.block : block_for_read(id, pg);
+    } else {
+      b = block_for_read(id, pg);
+    }
+    out.push_back(b);
+    wait_h2d = std::max(wait_h2d, blk_h2d_[static_cast<size_t>(b)]);
+  }
+}
+
 // -------------------------------------------------------------- logical ----
 void BlockPool::register_request(int64_t id, bool online) {
   Req r;

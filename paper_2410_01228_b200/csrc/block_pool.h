@@ -198,6 +198,10 @@ class BlockPool {
   // Block that attention should read for page idx of request id; counts
   // stale (non-resident) reads. -1 if the page never had a block.
   int32_t block_for_read(int64_t id, size_t page_idx);
+  // block_for_read of pages [0, n) appended to `out` with ONE request lookup
+  // (the plan build's hot loop: ~10K pages per decode step); also raises
+  // `wait_h2d` to the last restore writing any of those blocks
+  void blocks_for_read(int64_t id, size_t n, std::vector<int32_t>& out, int64_t& wait_h2d);
   int64_t n_blocks() const { return cfg_.n_blocks; }
   int64_t free_blocks() const { return static_cast<int64_t>(free_blocks_.size()); }
   int64_t quarantined_blocks() const { return static_cast<int64_t>(block_q_.size()); }

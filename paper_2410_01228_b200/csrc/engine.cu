@@ -1110,10 +1110,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
       ent_kvlen[i] = kv_len;
       ent_bt[i] = static_cast<int32_t>(bt.size());
       const int n_pages = (kv_len + 15) / 16;
-      for (int pg = 0; pg < n_pages; ++pg) {
-        bt.push_back(pool.block_for_read(be.request_id, static_cast<size_t>(pg)));
-        it.wait_h2d = std::max(it.wait_h2d, pool.block_h2d(bt.back()));
-      }
+      pool.blocks_for_read(be.request_id, static_cast<size_t>(n_pages), bt, it.wait_h2d);
       for (int32_t p : pos) {
         tok_ids.push_back(csk::token_id(e->cfg.token_seed, be.request_id, p, e->vocab));
         tok_pos.push_back(p);

@@ -104,12 +104,14 @@ __global__ void add_rmsnorm_kernel(__nv_bfloat16* x, const __nv_bfloat16* add, c
                                    const int32_t* row_idx, SafepointArg sp) {
   pdl_trigger();  // the next projection (K7) may start streaming its weights
   const int i = blockIdx.x;
-  if (i == 0 && threadIdx.x == 0) {
-    // rows of other CTAs may see the counts before or after the drop: a
-    // dropped row's norm is never read again, the next launch sees the cut
-    safepoint_check(const_cast<IterDesc*>(desc), sp);
+  if (sp.mb != nullptr && i == static_cast<int>(gridDim.x) - 1) {
+    // one extra CTA runs K6 (the mapped-mailbox read is a PCIe round trip)
+    // while the row CTAs normalise: rows may see the counts before or after
+    // the drop; a dropped row's norm is never read again, the next launch
+    // sees the cut
+    if (threadIdx.x == 0) safepoint_check(const_cast<IterDesc*>(desc), sp);
+    return;
   }
-  if (sp.mb != nullptr && sp.mode != 0) __syncthreads();  // CTA 0's own rows honour it
   int r;
   if (row_idx != nullptr) {
     if (i >= desc->n_ent_cur) return;
@@ -177,6 +179,7 @@ void add_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16
                  float eps, const IterDesc* desc, const int32_t* row_idx, int grid, cudaStream_t s,
                  const SafepointArg& sp) {
   if (grid <= 0) return;
+  if (sp.mb != nullptr) ++grid;  // + the K6 CTA
   const int vec = hidden / 8;
   // <= 512 threads: CH = ceil(vec / 512) chunks each (hidden <= 16384)
   const int threads = std::min(512, ((vec + 31) / 32) * 32);
