@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
 // counter, self-resetting). W and the pair layout come from the device
 // descriptor (n_dec_cur) and the page prefix sums, so a captured graph serves
 // every plan of its bucket and a safepoint drop re-balances the next layer.
-template <int D, int G>
+template <int D, int G, int NS>
 __global__ void __launch_bounds__(128, 3) attn_decode_sk_kernel(AttnParams p) {
   pdl_trigger();
   constexpr int KS = D / 16;
@@ -345,21 +345,28 @@ __global__ void __launch_bounds__(128, 3) attn_decode_sk_kernel(AttnParams p) {
     for (int k = 0; k < NTD; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
-    uint8_t* wbuf = smem + warp * 4 * PB;  // [stage][K|V]
+    // per-warp ring of NS pages (K and V): NS - 1 pages in flight while one
+    // is consumed
+    uint8_t* wbuf = smem + warp * NS * 2 * PB;  // [stage][K|V]
     int pg = pg0 + warp;
-    if (pg < pg1) {
-      load_page_async<D>(wbuf, wbuf + PB, kv_page(p, bt[pg], kvh, 0, D), kv_page(p, bt[pg], kvh, 1, D), lane);
+#pragma unroll
+    for (int s0 = 0; s0 < NS - 1; ++s0) {
+      const int pp = pg + 4 * s0;
+      if (pp < pg1) {
+        uint8_t* nb = wbuf + s0 * 2 * PB;
+        load_page_async<D>(nb, nb + PB, kv_page(p, bt[pp], kvh, 0, D), kv_page(p, bt[pp], kvh, 1, D), lane);
+      }
+      cp_async_commit();
     }
-    cp_async_commit();
     int stage = 0;
     for (; pg < pg1; pg += 4) {
-      const int nxt = pg + 4;
+      const int nxt = pg + 4 * (NS - 1);
       if (nxt < pg1) {
-        uint8_t* nb = wbuf + (stage ^ 1) * 2 * PB;
+        uint8_t* nb = wbuf + ((stage + NS - 1) % NS) * 2 * PB;
         load_page_async<D>(nb, nb + PB, kv_page(p, bt[nxt], kvh, 0, D), kv_page(p, bt[nxt], kvh, 1, D), lane);
       }
       cp_async_commit();
-      cp_async_wait<1>();
+      cp_async_wait<NS - 1>();
       __syncwarp();
       const uint8_t* sK = wbuf + stage * 2 * PB;
       const uint8_t* sV = sK + PB;
@@ -424,7 +431,7 @@ __global__ void __launch_bounds__(128, 3) attn_decode_sk_kernel(AttnParams p) {
         mma_bf16_16816(o[nd * 2 + 1], pa, v2, v3);
       }
       __syncwarp();
-      stage ^= 1;
+      stage = (stage + 1) % NS;
     }
     cp_async_wait<0>();
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
@@ -520,6 +527,10 @@ __global__ void __launch_bounds__(128, 3) attn_decode_sk_kernel(AttnParams p) {
 }
 
 // ------------------------------------------------------------- launchers ----
+int decode_sk_smem_bytes(int D, int ns) {
+  const int ring = 4 * ns * 2 * kPage * D * 2, merge = (4 * 16 * 2 + 4 * 16 * D) * 4;
+  return ring > merge ? ring : merge;
+}
 int decode_smem_bytes(int D) { return 4 * 4 * kPage * D * 2 > (4 * 16 * 2 + 4 * 16 * D) * 4 ? 4 * 4 * kPage * D * 2 : (4 * 16 * 2 + 4 * 16 * D) * 4; }
 
 bool launch_prefill_tc(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_pt_grid,
@@ -533,8 +544,14 @@ static void launch_attention_t(const AttnParams& p, const CUtensorMap* kv_map, i
   if (n_dec_grid > 0) {
     const int smem = decode_smem_bytes(D);
     if (p.sk_ctas > 0) {
-      smem_attr_once(reinterpret_cast<const void*>(attn_decode_sk_kernel<D, G>), smem);
-      attn_decode_sk_kernel<D, G><<<p.sk_ctas, 128, smem, s>>>(p);
+      if (p.sk_stages == 3) {
+        const int sm3 = decode_sk_smem_bytes(D, 3);
+        smem_attr_once(reinterpret_cast<const void*>(attn_decode_sk_kernel<D, G, 3>), sm3);
+        attn_decode_sk_kernel<D, G, 3><<<p.sk_ctas, 128, sm3, s>>>(p);
+      } else {
+        smem_attr_once(reinterpret_cast<const void*>(attn_decode_sk_kernel<D, G, 2>), smem);
+        attn_decode_sk_kernel<D, G, 2><<<p.sk_ctas, 128, smem, s>>>(p);
+      }
     } else {
       smem_attr_once(reinterpret_cast<const void*>(attn_decode_kernel<D, G>), smem);
       dim3 grid(p.n_splits, p.hkv, n_dec_grid);
@@ -547,13 +564,18 @@ static void launch_attention_t(const AttnParams& p, const CUtensorMap* kv_map, i
 }
 
 // Resident CTAs of the stream-K decode kernel per SM (its grid = this x SMs).
-int decode_sk_ctas_per_sm(int head_dim, int group) {
+int decode_sk_ctas_per_sm(int head_dim, int group, int ns) {
   int n = 0;
-  const int smem = decode_smem_bytes(head_dim);
+  const int smem = decode_sk_smem_bytes(head_dim, ns);
 #define CS_SK_OCC(DD, GG)                                                                                 \
   if (head_dim == DD && group == GG) {                                                                    \
-    smem_attr_once(reinterpret_cast<const void*>(attn_decode_sk_kernel<DD, GG>), smem);                   \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, attn_decode_sk_kernel<DD, GG>, 128, smem);          \
+    if (ns == 3) {                                                                                        \
+      smem_attr_once(reinterpret_cast<const void*>(attn_decode_sk_kernel<DD, GG, 3>), smem);              \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, attn_decode_sk_kernel<DD, GG, 3>, 128, smem);     \
+    } else {                                                                                              \
+      smem_attr_once(reinterpret_cast<const void*>(attn_decode_sk_kernel<DD, GG, 2>), smem);              \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, attn_decode_sk_kernel<DD, GG, 2>, 128, smem);     \
+    }                                                                                                     \
   }
   CS_SK_OCC(64, 1)
   CS_SK_OCC(64, 2)

@@ -109,6 +109,7 @@ struct AttnParams {
   const int32_t* dec_pfx;       // [n_dec + 1] K1 stream-K: prefix sums of the decode entries' page counts
   float* ws_sk;                 // K1 stream-K partials [cta][2] x {m[G], l[G], O[G][D]}
   int32_t sk_ctas;              // K1 stream-K grid (0: the split-K kernel)
+  int32_t sk_stages;            // K1 stream-K per-warp ring depth (2 or 3)
   int32_t k2_splits, k2_tiles_per_split;  // K2: splits over 128-key tiles
   int32_t k2_pair;                        // K2 on CTA pairs (attn_tc2.cu, head_dim 128)
   float scale_log2;             // softmax_scale * log2(e)

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cctype>
+#include <chrono>
 #include <cmath>
 #include <array>
 #include <atomic>
@@ -64,7 +65,7 @@ void kv_move(bool to_host, __nv_bfloat16* pool, __nv_bfloat16* host_mapped, cons
 void kv_pack(bool to_stage, __nv_bfloat16* pool, __nv_bfloat16* stage, const void* segs, const int64_t* stage_off,
              int n_segs, int runs_per_seg, int D, int sms, cudaStream_t s);
 void fill_pool(__nv_bfloat16* pool, size_t n, uint64_t seed, cudaStream_t s);
-int decode_sk_ctas_per_sm(int head_dim, int group);
+int decode_sk_ctas_per_sm(int head_dim, int group, int ns);
 bool launch_attention(const AttnParams& p, const CUtensorMap* kv_map, int head_dim, int group, int n_dec_grid,
                       int n_pt_grid, cudaStream_t s);
 int prefill_tile_rows();
@@ -260,6 +261,10 @@ struct cs_engine {
   int32_t* dec_cnt = nullptr;  // K1 split-K arrival counters
   float* ws_sk = nullptr;      // K1 stream-K partials
   int sk_ctas = 0;             // K1 stream-K grid (0: split-K kernel)
+  int sk_stages = 2;           // K1 stream-K per-warp ring depth (CS_K1_STAGES=3 for A/B)
+  // host time per forward (CS_HOST_TIMERS=1 prints the totals at cs_destroy)
+  double host_prep_ms = 0, host_enq_ms = 0, host_wait_ms = 0, host_post_ms = 0;
+  int64_t host_launches = 0;
   bool k2_pair = false;        // K2 on CTA pairs (head_dim 128; opt-in CS_K2_PAIR=1)
   size_t ws2_floats = 0;
   uint8_t* d_meta = nullptr;
@@ -1057,6 +1062,10 @@ void cs_engine::enqueue_layers() {
 
 // Builds the iteration's device metadata into the pinned
 // staging buffer and the attention parameters; false for bookkeeping-only.
+static double host_ms_now() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32_t n, uint64_t epoch) {
     if (e->it.active) throw std::logic_error("iterations overlap on the device");
     if (n < 1) throw std::invalid_argument("empty batch");
@@ -1323,6 +1332,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     // (profiles/r2/k1_streamk_ab.md). Graphs are keyed by the choice.
     it.k1_sk = e->sk_ctas > 0 && it.n_dec * e->hkv < e->sk_ctas;
     ap.sk_ctas = it.k1_sk ? e->sk_ctas : 0;
+    ap.sk_stages = e->sk_stages;
     ap.tiles = reinterpret_cast<const csk::PrefillTile*>(d + o_tiles);
     ap.tile_order = reinterpret_cast<const int32_t*>(d + o_tiles + sizeof(csk::PrefillTile) * tiles.size());
     ap.ws = e->ws;
@@ -1570,7 +1580,9 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
           const char* k2s = std::getenv("CS_K2_PAIR");
           e->k2_pair = e->D == 128 && k2s && k2s[0] == '1';
           const char* sk = std::getenv("CS_K1_SPLITK");
-          if (!(sk && sk[0] == '1')) e->sk_ctas = csk::decode_sk_ctas_per_sm(e->D, e->G) * e->sms;
+          const char* st = std::getenv("CS_K1_STAGES");
+          e->sk_stages = st && st[0] == '3' ? 3 : 2;
+          if (!(sk && sk[0] == '1')) e->sk_ctas = csk::decode_sk_ctas_per_sm(e->D, e->G, e->sk_stages) * e->sms;
           if (e->sk_ctas > 0) {
             const size_t n = static_cast<size_t>(e->sk_ctas) * 2 * e->G * (e->D + 2);
             CK(cudaMalloc(&e->ws_sk, n * 4));
@@ -1656,6 +1668,12 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
 
 int cs_destroy(cs_engine* e) {
   if (!e) return CS_OK;
+  if (std::getenv("CS_HOST_TIMERS") && e->host_launches > 0)
+    std::fprintf(stderr,
+                 "{\"host_timers\": {\"forwards\": %lld, \"prepare_ms\": %.1f, \"enqueue_ms\": %.1f, "
+                 "\"wait_ms\": %.1f, \"post_ms\": %.1f}}\n",
+                 static_cast<long long>(e->host_launches), e->host_prep_ms, e->host_enq_ms, e->host_wait_ms,
+                 e->host_post_ms);
   return guard([&] {
     if (!e->host_only) {
       cudaDeviceSynchronize();
@@ -1957,7 +1975,10 @@ int cs_kv_block_table(cs_engine* e, int64_t id, int32_t* blocks, int32_t* slots,
 // ---------------------------------------------------------------- forward --
 int cs_forward_launch(cs_engine* e, const cs_batch_entry* entries, int32_t n, uint64_t epoch) {
   const int rc = guard([&] {
+    const double h0 = host_ms_now();
     if (!prepare_iteration(e, entries, n, epoch)) return;
+    const double h1 = host_ms_now();
+    e->host_prep_ms += h1 - h0;
     auto& it = e->it;
     // restores the reference already counts complete may still be copying:
     // the forward (not the host) waits for the ones writing blocks it reads
@@ -1971,6 +1992,8 @@ int cs_forward_launch(cs_engine* e, const cs_batch_entry* entries, int32_t n, ui
     it.active = true;
     it.device_m = e->use_pf(it.n_tok, (e->hq + 2 * e->hkv) * e->D, e->hidden) && !it.graph;
     e->enqueue_layers();
+    e->host_enq_ms += host_ms_now() - h1;
+    ++e->host_launches;
   });
   if (rc != CS_OK && e->it.active) {  // balance the pool's forward counters
     e->it.active = false;
@@ -2171,8 +2194,11 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
     inf.preempted_at_layer = -1;
     inf.gemm_trunc_layer = -1;
     int n_alive = it.n_ent;
+    const double w0 = host_ms_now();
+    double w1 = w0;
     if (!(e->host_only || e->no_model || e->dry)) {
       CK(cudaEventSynchronize(e->ev_end));
+      w1 = host_ms_now();
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, e->ev_start, e->ev_end));
       inf.gpu_ms = ms;
@@ -2241,6 +2267,8 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
     e->pool->on_forward_completed();
     it.active = false;
     if (info) *info = inf;
+    e->host_wait_ms += w1 - w0;
+    e->host_post_ms += host_ms_now() - w1;
   });
 }
 

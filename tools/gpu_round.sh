@@ -51,6 +51,19 @@ if has k2ab; then
   CS_K2_PAIR=1 timeout 600 python tools/k2_sweep.py 20 > "$OUT/k2_pair.jsonl" 2> "$OUT/k2_pair.err"
   CS_K2_PAIR=1 timeout 600 python -m pytest tests/test_gpu_attention.py -x -q > "$OUT/pytest_attention_pair.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_attention_pair.log"
 fi
+if has k1st; then
+  timeout 600 python -m pytest tests/test_gpu_attention.py -x -q > "$OUT/pytest_attention.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_attention.log"
+  CS_K1_STAGES=3 timeout 600 python -m pytest tests/test_gpu_attention.py -x -q -k k1 > "$OUT/pytest_attention3.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_attention3.log"
+  for shape in "39 4237" "8 4237" "16 16000" "24 4000"; do
+    for st in 2 3; do
+      CS_K1_STAGES=$st timeout 300 python tools/decode_probe.py $shape 8 >> "$OUT/k1st.jsonl" 2>> "$OUT/k1st.err"
+      echo "{\"stages\": $st, \"shape\": \"$shape\"}" >> "$OUT/k1st.jsonl"
+    done
+  done
+fi
+if has hosttimers; then
+  CS_HOST_TIMERS=1 timeout 900 python bench.py --no-probes --legs "" > "$OUT/bench_ht.json" 2> "$OUT/bench_ht.err"
+fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
