@@ -2197,7 +2197,14 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
     const double w0 = host_ms_now();
     double w1 = w0;
     if (!(e->host_only || e->no_model || e->dry)) {
-      CK(cudaEventSynchronize(e->ev_end));
+      // spin on the event (the iteration's end is the host loop's critical
+      // path: a yielding/blocking wait adds its wake-up latency to every
+      // iteration of the serving loop)
+      for (;;) {
+        const cudaError_t q = cudaEventQuery(e->ev_end);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) CK(q);
+      }
       w1 = host_ms_now();
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, e->ev_start, e->ev_end));

@@ -64,6 +64,9 @@ fi
 if has hosttimers; then
   CS_HOST_TIMERS=1 timeout 900 python bench.py --no-probes --legs "" > "$OUT/bench_ht.json" 2> "$OUT/bench_ht.err"
 fi
+if has stream; then
+  timeout 300 ./tools/stream_bench > "$OUT/stream_bench.jsonl" 2>&1
+fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
