@@ -1980,12 +1980,14 @@ int cs_forward_launch(cs_engine* e, const cs_batch_entry* entries, int32_t n, ui
     const double h1 = host_ms_now();
     e->host_prep_ms += h1 - h0;
     auto& it = e->it;
+    // the forward's device time starts here, so a stall on a restore below
+    // counts as time of this iteration
+    CK(cudaEventRecord(e->ev_start, e->s_compute));
     // restores the reference already counts complete may still be copying:
     // the forward (not the host) waits for the ones writing blocks it reads
     if (it.wait_h2d > 0 && e->mover && e->mover->done_prefix(CS_H2D) < it.wait_h2d) {
       if (cudaEvent_t w = e->mover->pending_event(CS_H2D, it.wait_h2d)) CK(cudaStreamWaitEvent(e->s_compute, w, 0));
     }
-    CK(cudaEventRecord(e->ev_start, e->s_compute));
     CK(cudaMemcpyAsync(e->d_meta, e->h_meta, static_cast<size_t>(it.meta_bytes), cudaMemcpyHostToDevice,
                        e->s_compute));
     e->any_forward = true;

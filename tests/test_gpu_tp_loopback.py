@@ -47,11 +47,14 @@ def _in_child(case, tp=2, mode="auto"):
 
 SHAPE = dict(num_layers=4, hidden=256, n_heads=8, n_kv_heads=4, head_dim=64, ffn=512, vocab=512,
              max_batched_tokens=1024, gpu_kv_capacity=4096 * 16 * 2 * 4 * 64 * 2 * 4, safepoint_interval_layers=1)
+# g = 8 needs 8 KV heads (one per rank), as the three target models have
+SHAPE8 = dict(SHAPE, n_kv_heads=8, gpu_kv_capacity=4096 * 16 * 2 * 8 * 64 * 2 * 4)
 
 
 def _engines(instrumented=0, tp=2):
-    full = cs.Engine(cs.model_config("tiny", instrumented=instrumented, **SHAPE))
-    ranks = [cs.Engine(cs.model_config("tiny", instrumented=instrumented, tp_size=tp, tp_rank=r, **SHAPE))
+    shape = SHAPE8 if tp == 8 else SHAPE
+    full = cs.Engine(cs.model_config("tiny", instrumented=instrumented, **shape))
+    ranks = [cs.Engine(cs.model_config("tiny", instrumented=instrumented, tp_size=tp, tp_rank=r, **shape))
              for r in range(tp)]
     ptrs = []
     for e in ranks:
@@ -87,7 +90,7 @@ def test_flag_on_one_rank_drops_both_at_the_same_layer():
     _in_child("flag")
 
 
-@pytest.mark.parametrize("tp,mode", [(2, "twoshot"), (4, "oneshot"), (4, "twoshot")])
+@pytest.mark.parametrize("tp,mode", [(2, "twoshot"), (4, "oneshot"), (4, "twoshot"), (8, "oneshot"), (8, "twoshot")])
 def test_ranks_match_unsharded_per_allreduce_kernel(tp, mode):
     """The two-shot (reduce-scatter + all-gather) peer kernel gives the same
     bits as the one-shot kernel's fold order; tp=4 exercises uneven chunks."""
