@@ -115,6 +115,20 @@ struct AttnParams {
   float scale_log2;             // softmax_scale * log2(e)
 };
 
+// K8 epilogue fusions (gemm_pf.cu), tp = 1 prefill layers:
+//  * resid: y = x + acc -- the residual add of the next RMSNorm, written in
+//    place over x (bit-identical to storing acc as bf16 and adding after);
+//  * rope: the qkv projection's q / k heads rotated (RoPE, (cos, sin) from a
+//    per-iteration [token][D/2] table) and k / v scattered into the KV pool
+//    at each token's (block, slot) -- bit-identical to rope_append.
+struct PfExtra {
+  __nv_bfloat16* resid = nullptr;     // x [M, N] bf16, updated in place (y unused)
+  const float2* rope_tab = nullptr;   // [token][D/2] (cos, sin); null: no rope
+  const int32_t* tok_slot = nullptr;  // [token] block * 16 + slot
+  __nv_bfloat16* pool = nullptr;
+  int32_t hq = 0, hkv = 0, D = 0, num_layers = 0, layer = 0;
+};
+
 // Peer-memory all-reduce arguments (kernels.cu p2p_allreduce): for each of
 // the g ranks, the partial buffer of this step and its exchange-region words.
 struct P2PArgs {

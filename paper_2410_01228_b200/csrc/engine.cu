@@ -82,7 +82,9 @@ void p2p_allreduce(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int bloc
 void p2p_allreduce2(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s);
 bool gemm_pf_supported(int N, int K);
 void gemm_pf(const CUtensorMap* xmap, const CUtensorMap* wmap, void* y, int M, const int32_t* m_dev, int N, int K,
-             bool f32_out, int sms, cudaStream_t s, bool swiglu = false);
+             bool f32_out, int sms, cudaStream_t s, bool swiglu = false, const PfExtra* ex = nullptr);
+void rope_table(float2* tab, const int32_t* tok_pos, int D, float theta, const IterDesc* desc, int grid,
+                cudaStream_t s);
 }  // namespace csk
 
 namespace {
@@ -361,7 +363,9 @@ struct cs_engine {
     ++graph_gen;
   }
   int gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32,
-           const int32_t* m_dev = nullptr);
+           const int32_t* m_dev = nullptr, const csk::PfExtra* ex = nullptr);
+  float2* rope_tab = nullptr;  // [max_tok][D/2] (cos, sin) of the iteration (K8 qkv epilogue)
+  bool fuse_epilogues = true;  // K8 RoPE / residual epilogues (CS_NO_FUSE=1: separate kernels, for A/B)
   // Per-kernel-class device timing (cs_set_kernel_timing; bench roofline):
   // event pairs on the launching stream around every non-graph launch of
   // K8 / K2 / K1, folded into the totals at cs_iter_wait (iterations the
@@ -861,17 +865,21 @@ bool cs_engine::use_pf(int M, int N, int K) const {
 // Returns the number of hand-written kernels it launched (K7/K8: 1, cuBLAS: 0).
 // m_dev: device row count (IterDesc.n_tok_cur) honoured by K8.
 int cs_engine::gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32,
-                    const int32_t* m_dev) {
+                    const int32_t* m_dev, const csk::PfExtra* ex) {
   if (M <= 0) return 0;
+  // an epilogue fusion is only requested where K8 runs (use_pf checked by the caller)
+  if (ex && !use_pf(M, N, K)) throw std::logic_error("K8 epilogue fusion requested off the K8 path");
   if (use_pf(M, N, K)) {
     const int rows = A == xl ? static_cast<int>(max_ent) : static_cast<int>(max_tok);
     const CUtensorMap* xm = tmap(A, rows, K, 128);
     const CUtensorMap* wm = tmap(W, N, K, 128);
     if (xm && wm) {
-      timed(CS_KT_K8, 2.0 * M * N * K, [&] { csk::gemm_pf(xm, wm, C, M, m_dev, N, K, out_f32, sms, s_compute); });
+      timed(CS_KT_K8, 2.0 * M * N * K,
+            [&] { csk::gemm_pf(xm, wm, C, M, m_dev, N, K, out_f32, sms, s_compute, false, ex); });
       return 1;
     }
   }
+  if (ex) throw CudaError("K8 tensor maps unavailable for a fused epilogue");
   if (wgemm(A, W, C, M, N, K, out_f32)) return 1;
   timed(CS_KT_LIB, 2.0 * M * N * K, [&] {
     if (lt_gemm(A, W, C, M, N, K, out_f32)) return;
@@ -932,6 +940,16 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   __nv_bfloat16* tail = tmp + static_cast<size_t>(max_tok) * hidden;  // vote slot
   auto is_sp = [&](int l) { return instrumented && l > 0 && l < L && l % cfg.safepoint_interval_layers == 0; };
 
+  // K8 epilogue fusions (single rank, K8 path): RoPE + KV append in the qkv
+  // projection, the residual add in o_proj / down
+  const bool fuse_ok = !graph && tp == 1 && fuse_epilogues;
+  const bool fuse_rope = fuse_ok && D == 128 && rope_tab && use_pf(static_cast<int>(Tg), qkv_cols, hidden);
+  const bool fuse_o = fuse_ok && use_pf(static_cast<int>(Tg), hidden, hq * D);
+  const bool fuse_down = fuse_ok && use_pf(static_cast<int>(Tg), hidden, ffn);
+  if (fuse_rope) {
+    csk::rope_table(rope_tab, it.ap.tok_pos, D, cfg.rope_theta, desc, T, s_compute);
+    ++n_launch;
+  }
   for (int l = 0; l < L; ++l) {
     const int64_t M = Tg;
     if (l == 0) {
@@ -946,11 +964,24 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
       sp.mode = is_sp(l) ? (tp == 1 ? 1 : 2) : 0;
       sp.tail = tail;
     }
-    csk::add_rmsnorm(x, l == 0 ? nullptr : tmp, w.attn_norm[l], xn, hidden, cfg.rms_eps, desc, nullptr, T, s_compute,
-                     sp);
-    n_launch += gemm(xn, w.wqkv[l], qkv, static_cast<int>(M), qkv_cols, hidden, false, m_dev);
-    csk::rope_append(qkv, it.ap.tok_pos, it.d_tok_slot, kv, hq, hkv, D, L, l,
-                     cfg.rope_theta, desc, T, s_compute);
+    csk::add_rmsnorm(x, (l == 0 || fuse_down) ? nullptr : tmp, w.attn_norm[l], xn, hidden, cfg.rms_eps, desc,
+                     nullptr, T, s_compute, sp);
+    if (fuse_rope) {
+      csk::PfExtra ex;
+      ex.rope_tab = rope_tab;
+      ex.tok_slot = it.d_tok_slot;
+      ex.pool = kv;
+      ex.hq = hq;
+      ex.hkv = hkv;
+      ex.D = D;
+      ex.num_layers = L;
+      ex.layer = l;
+      n_launch += gemm(xn, w.wqkv[l], qkv, static_cast<int>(M), qkv_cols, hidden, false, m_dev, &ex);
+    } else {
+      n_launch += gemm(xn, w.wqkv[l], qkv, static_cast<int>(M), qkv_cols, hidden, false, m_dev);
+      csk::rope_append(qkv, it.ap.tok_pos, it.d_tok_slot, kv, hq, hkv, D, L, l,
+                       cfg.rope_theta, desc, T, s_compute);
+    }
     csk::AttnParams ap = it.ap;
     ap.layer = l;
     bool ok = true;
@@ -960,13 +991,17 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
     if (it.n_pt > 0)
       timed(CS_KT_K2, it.k2_flops, [&] { ok &= csk::launch_attention(ap, &kv_map, D, G, 0, it.n_pt, s_compute); });
     if (!ok) throw ConfigError("unsupported attention shape");
-    {
+    if (fuse_o) {  // x += attn . Wo^T in K8's epilogue
+      csk::PfExtra ex;
+      ex.resid = x;
+      n_launch += gemm(attn, w.wo[l], tmp, static_cast<int>(M), hidden, hq * D, false, m_dev, &ex);
+    } else {
       __nv_bfloat16* part = partial_out(tmp);
       n_launch += gemm(attn, w.wo[l], part, static_cast<int>(M), hidden, hq * D, false, m_dev);
       if (part != tmp) ++n_launch;
       reduce_into(tmp, M * hidden);
     }
-    csk::add_rmsnorm(x, tmp, w.mlp_norm[l], xn, hidden, cfg.rms_eps, desc, nullptr, T, s_compute);
+    csk::add_rmsnorm(x, fuse_o ? nullptr : tmp, w.mlp_norm[l], xn, hidden, cfg.rms_eps, desc, nullptr, T, s_compute);
     const CUtensorMap* gxm = nullptr;
     const CUtensorMap* gwm = nullptr;
     if (gu_interleave && use_pf(static_cast<int>(M), 2 * ffn, hidden)) {
@@ -983,7 +1018,11 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
       csk::silu_mul(gu, act, ffn, desc, T, s_compute, gu_interleave);
       n_launch += 1;
     }
-    {
+    if (fuse_down) {  // x += act . Wd^T in K8's epilogue
+      csk::PfExtra ex;
+      ex.resid = x;
+      n_launch += gemm(act, w.wd[l], tmp, static_cast<int>(M), hidden, ffn, false, m_dev, &ex);
+    } else {
       __nv_bfloat16* part = partial_out(tmp);
       n_launch += gemm(act, w.wd[l], part, static_cast<int>(M), hidden, ffn, false, m_dev);
       if (tp > 1) {
@@ -998,7 +1037,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
         }
       }
     }
-    n_launch += (l == 0 ? 1 : 0) + 3 + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
+    n_launch += (l == 0 ? 1 : 0) + 3 - (fuse_rope ? 1 : 0) + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
                 (it.n_dec > 0 ? 1 : 0) + (it.n_pt > 0 ? (it.k2_splits > 1 ? 2 : 1) : 0);
     if ((cfg.flags & CS_FLAG_SYNC_DEBUG) && !graph) {
       CK(cudaStreamSynchronize(s_compute));
@@ -1007,7 +1046,8 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   }
   // Final norm of each entry's last row -> lm_head -> argmax.
   const int E = Eg;
-  csk::add_rmsnorm(x, tmp, w.final_norm, xl, hidden, cfg.rms_eps, desc, it.d_ent_last, E, s_compute);
+  csk::add_rmsnorm(x, fuse_down ? nullptr : tmp, w.final_norm, xl, hidden, cfg.rms_eps, desc, it.d_ent_last, E,
+                   s_compute);
   n_launch += gemm(xl, w.lm_head, logits, E, vocab, hidden, true);
   csk::argmax_rows(logits, vocab, reinterpret_cast<unsigned long long*>(d_out + sizeof(csk::IterDesc)), desc, E,
                    s_compute);
@@ -1598,6 +1638,9 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         {
           // K7 for the M <= 256 projections: 2 (default) where start-up
           // tuning timed it faster than the best cuBLAS plan, 1 always, 0 never
+          const char* nf = std::getenv("CS_NO_FUSE");
+          e->fuse_epilogues = !(nf && nf[0] == '1');
+          if (e->D == 128) CK(cudaMalloc(&e->rope_tab, static_cast<size_t>(e->max_tok) * (e->D / 2) * sizeof(float2)));
           const char* ksk = std::getenv("CS_K7_SK");
           e->k7_sk = ksk && ksk[0] == '1';
           const char* v = std::getenv("CS_WGEMM");
@@ -1703,6 +1746,7 @@ int cs_destroy(cs_engine* e) {
                       static_cast<void*>(e->act), static_cast<void*>(e->xl), static_cast<void*>(e->logits),
                       static_cast<void*>(e->ws), static_cast<void*>(e->ws2), static_cast<void*>(e->dec_cnt),
                       static_cast<void*>(e->ws_sk), static_cast<void*>(e->k7_ws), static_cast<void*>(e->k7_cnt),
+                      static_cast<void*>(e->rope_tab),
                       static_cast<void*>(e->d_meta),
                       static_cast<void*>(e->d_out),
                       e->blas_ws})

@@ -50,6 +50,7 @@ struct PfArgs {
   int32_t f32_out;
   int32_t band;          // m-tiles per raster band (L2 reuse of the X and W panels)
   int32_t swiglu;        // W = gate|up interleaved in 128-row blocks: y = silu(gate) * up [M, N / 2]
+  PfExtra ex;            // fused residual add / RoPE + KV append (common.cuh)
 };
 
 // Tile t -> (m tile, n tile): bands of `band` m-tiles, m fastest inside a
@@ -208,13 +209,91 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         if (lane == 0) tc::mbar_arrive_cluster(tempty0 + acc * 8);
         continue;
       }
+      if (a.ex.rope_tab != nullptr) {
+        // qkv + RoPE + KV append: this 256-column tile = two heads of 128
+        // (q heads rotated in place in y; k heads rotated and v heads copied
+        // into the pool). Values are rounded to bf16 first, as the unfused
+        // path stores qkv, then rotated exactly as rope_append does.
+        const int D = 128, half = 64;
+        int slot = 0, blk = 0, off = 0;
+        if (row < M) {
+          slot = a.ex.tok_slot[row];
+          blk = slot >> 4;
+          off = slot & 15;
+        }
+        const size_t layer_elems = static_cast<size_t>(2) * a.ex.hkv * 16 * D;
+        __nv_bfloat16* kv_base = a.ex.pool + (static_cast<size_t>(blk) * a.ex.num_layers + a.ex.layer) * layer_elems;
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+          const int h = (n0 + hh * D) / D;  // head index in the q | k | v layout
+#pragma unroll 1
+          for (int jc = 0; jc < half; jc += 32) {
+            float va[32], vb[32];
+            tc::tmem_ld32(tl + hh * D + jc, va);
+            tc::tmem_ld32(tl + hh * D + half + jc, vb);
+            tc::tmem_wait_ld();
+            tc::reg_fence<32>(va);
+            tc::reg_fence<32>(vb);
+            if (row >= M) continue;
+            __nv_bfloat16* dst;
+            if (h < a.ex.hq) dst = static_cast<__nv_bfloat16*>(a.y) + static_cast<size_t>(row) * a.N + h * D;
+            else if (h < a.ex.hq + a.ex.hkv) dst = kv_base + (static_cast<size_t>(h - a.ex.hq) * 16 + off) * D;
+            else dst = kv_base + (static_cast<size_t>(a.ex.hkv + h - a.ex.hq - a.ex.hkv) * 16 + off) * D;
+            const bool rot = h < a.ex.hq + a.ex.hkv;
+            const float2* tab = a.ex.rope_tab + static_cast<size_t>(row) * half + jc;
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              uint32_t w1[4], w2[4];
+#pragma unroll
+              for (int k = 0; k < 8; k += 2) {
+                float y1[2], y2[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                  const float x1 = __bfloat162float(__float2bfloat16(va[j + k + u]));
+                  const float x2 = __bfloat162float(__float2bfloat16(vb[j + k + u]));
+                  if (rot) {  // the same operations as rope_append_kernel
+                    const float2 r = tab[j + k + u];
+                    y1[u] = __fmaf_rn(x1, r.x, -__fmul_rn(x2, r.y));
+                    y2[u] = __fmaf_rn(x2, r.x, __fmul_rn(x1, r.y));
+                  } else {
+                    y1[u] = x1;
+                    y2[u] = x2;
+                  }
+                }
+                w1[k / 2] = pack_bf16(y1[0], y1[1]);
+                w2[k / 2] = pack_bf16(y2[0], y2[1]);
+              }
+              *reinterpret_cast<uint4*>(dst + jc + j) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+              *reinterpret_cast<uint4*>(dst + half + jc + j) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+            }
+          }
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_cluster(tempty0 + acc * 8);
+        continue;
+      }
 #pragma unroll 1
       for (int c = 0; c < kPfN; c += 32) {
         float v[32];
         tc::tmem_ld32(tl + c, v);
         tc::tmem_wait_ld();
         tc::reg_fence<32>(v);
-        if (row < M) {
+        if (row < M && a.ex.resid != nullptr) {
+          // residual add fused: x = x + bf16(acc), in place
+          uint4* xr = reinterpret_cast<uint4*>(a.ex.resid + static_cast<size_t>(row) * a.N + n0 + c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 xo = xr[j];
+            const __nv_bfloat16* xe = reinterpret_cast<const __nv_bfloat16*>(&xo);
+            float o[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+              o[t] = __bfloat162float(xe[t]) + __bfloat162float(__float2bfloat16(v[8 * j + t]));
+            xr[j] = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]),
+                               pack_bf16(o[6], o[7]));
+          }
+        } else if (row < M) {
           if (a.f32_out) {
             float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.y) + static_cast<size_t>(row) * a.N + n0 + c);
 #pragma unroll
@@ -249,9 +328,10 @@ int gemm_pf_rows_box() { return kPfRows; }
 // [N][K], both 64 x 128 boxes with 128-B swizzle. M is the host bound (grid
 // size); m_dev, when set, the live row count read by the kernel.
 void gemm_pf(const CUtensorMap* xmap, const CUtensorMap* wmap, void* y, int M, const int32_t* m_dev, int N, int K,
-             bool f32_out, int sms, cudaStream_t s, bool swiglu) {
+             bool f32_out, int sms, cudaStream_t s, bool swiglu, const PfExtra* ex) {
   smem_attr_once(reinterpret_cast<const void*>(gemm_pf_kernel), kPfSmem);
   PfArgs a{};
+  if (ex) a.ex = *ex;
   a.y = y;
   a.m_dev = m_dev;
   a.M = M;

@@ -273,8 +273,12 @@ __global__ void __launch_bounds__(128) rope_append_kernel(__nv_bfloat16* qkv, co
       const float2 a = __bfloat1622float2(a2[k]);
       const float2 b = __bfloat1622float2(b2[k]);
       const float2 r0 = rot[j + 2 * k], r1 = rot[j + 2 * k + 1];
-      y1[k] = __floats2bfloat162_rn(a.x * r0.x - b.x * r0.y, a.y * r1.x - b.y * r1.y);
-      y2[k] = __floats2bfloat162_rn(b.x * r0.x + a.x * r0.y, b.y * r1.x + a.y * r1.y);
+      // explicit fma / mul (no contraction choice left to the compiler): the
+      // K8 qkv epilogue (gemm_pf.cu) rotates with the same operations
+      y1[k] = __floats2bfloat162_rn(__fmaf_rn(a.x, r0.x, -__fmul_rn(b.x, r0.y)),
+                                    __fmaf_rn(a.y, r1.x, -__fmul_rn(b.y, r1.y)));
+      y2[k] = __floats2bfloat162_rn(__fmaf_rn(b.x, r0.x, __fmul_rn(a.x, r0.y)),
+                                    __fmaf_rn(b.y, r1.x, __fmul_rn(a.y, r1.y)));
     }
     __nv_bfloat16* dst = h < hq ? hp : kv_base + (static_cast<size_t>(h - hq) * 16 + off) * D;
     *reinterpret_cast<uint4*>(dst + j) = uy1;
@@ -287,6 +291,27 @@ __global__ void __launch_bounds__(128) rope_append_kernel(__nv_bfloat16* qkv, co
     __nv_bfloat16* dst = kv_base + (static_cast<size_t>(hkv + h) * 16 + off) * D + d;
     *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v + h * D + d);
   }
+}
+
+// (cos, sin) of every (token, frequency) of the iteration, [token][D/2]:
+// positions are the same in every layer, so the K8 qkv epilogue reads this
+// table instead of evaluating sincos per head. Same expressions as
+// rope_append_kernel (bit-identical angles).
+__global__ void rope_table_kernel(float2* tab, const int32_t* tok_pos, int D, float theta, const IterDesc* desc) {
+  const int t = blockIdx.x;
+  if (t >= desc->n_tok_all) return;
+  const float pos = static_cast<float>(tok_pos[t]);
+  for (int j = threadIdx.x; j < D / 2; j += blockDim.x) {
+    const float inv_freq = powf(theta, -2.f * static_cast<float>(j) / static_cast<float>(D));
+    float sn, cs;
+    sincosf(pos * inv_freq, &sn, &cs);
+    tab[static_cast<size_t>(t) * (D / 2) + j] = make_float2(cs, sn);
+  }
+}
+
+void rope_table(float2* tab, const int32_t* tok_pos, int D, float theta, const IterDesc* desc, int grid,
+                cudaStream_t s) {
+  if (grid > 0) rope_table_kernel<<<grid, 64, 0, s>>>(tab, tok_pos, D, theta, desc);
 }
 
 void rope_append(__nv_bfloat16* qkv, const int32_t* tok_pos, const int32_t* tok_slot, __nv_bfloat16* pool, int hq,
