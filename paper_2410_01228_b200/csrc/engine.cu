@@ -1808,8 +1808,9 @@ static void attach_common(cs_engine* e, const std::vector<uint8_t*>& peers, bool
   e->p2p = true;
   e->part_slot = 0;
   // same-device (loopback) peers run concurrently with this kernel's
-  // spinning blocks: keep it small so the other rank's kernels get SMs
-  e->p2p_blocks = same_device ? 16 : 2 * e->sms;
+  // spinning blocks: keep all ranks' spinners together at <= 32 CTAs so the
+  // ranks still behind get SMs for their layer kernels
+  e->p2p_blocks = same_device ? std::max(2, 32 / e->tp) : 2 * e->sms;
   if (const char* m = std::getenv("CS_P2P_ALLREDUCE")) {
     e->p2p_mode = std::strcmp(m, "twoshot") == 0 ? 2 : std::strcmp(m, "oneshot") == 0 ? 1 : 0;
   }
