@@ -17,7 +17,7 @@ if has smoke; then timeout 300 python -c "import __graft_entry__ as g; g.smoke()
 if has tests; then timeout 900 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_gpu.log"; fi
 if has bench; then timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/bench.err"; fi
 NCU="ncu --clock-control none"
-if has tptests; then timeout 900 python -m pytest tests/test_gpu_tp_loopback.py tests/test_gpu_tp_ipc.py tests/test_gpu_ckpt.py tests/test_gpu_hostpool.py -x -q > "$OUT/pytest_tp_ckpt.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_tp_ckpt.log"; fi
+if has tptests; then timeout 900 python -m pytest tests/test_gpu_tp_loopback.py tests/test_gpu_tp_ipc.py tests/test_gpu_ckpt.py tests/test_gpu_hostpool.py tests/test_gpu_fusion.py -q > "$OUT/pytest_tp_ckpt.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_tp_ckpt.log"; fi
 if has decode; then
   timeout 300 python tools/decode_probe.py 39 4237 12 > "$OUT/decode_probe.json" 2> "$OUT/decode_probe.err"
   timeout 600 $NCU --metrics gpu__time_duration.sum --csv --log-file "$OUT/decode_launches.csv" \
