@@ -263,6 +263,7 @@ struct cs_engine {
   int32_t* dec_cnt = nullptr;  // K1 split-K arrival counters
   float* ws_sk = nullptr;      // K1 stream-K partials
   int sk_ctas = 0;             // K1 stream-K grid (0: split-K kernel)
+  int sk_resident = 0;         // K1 stream-K CTAs resident at once (the kernel choice threshold)
   int sk_stages = 2;           // K1 stream-K per-warp ring depth (CS_K1_STAGES=3 for A/B)
   // host time per forward (CS_HOST_TIMERS=1 prints the totals at cs_destroy)
   double host_prep_ms = 0, host_enq_ms = 0, host_wait_ms = 0, host_post_ms = 0;
@@ -1370,7 +1371,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     // SMs streaming (39 x 4.2K: -3.3% step time); with more pairs the
     // per-pair split-K kernel has no segment overhead (128 x 2K: -5.5%)
     // (profiles/r2/k1_streamk_ab.md). Graphs are keyed by the choice.
-    it.k1_sk = e->sk_ctas > 0 && it.n_dec * e->hkv < e->sk_ctas;
+    it.k1_sk = e->sk_ctas > 0 && it.n_dec * e->hkv < e->sk_resident;
     ap.sk_ctas = it.k1_sk ? e->sk_ctas : 0;
     ap.sk_stages = e->sk_stages;
     ap.tiles = reinterpret_cast<const csk::PrefillTile*>(d + o_tiles);
@@ -1622,7 +1623,14 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
           const char* sk = std::getenv("CS_K1_SPLITK");
           const char* st = std::getenv("CS_K1_STAGES");
           e->sk_stages = st && st[0] == '3' ? 3 : 2;
-          if (!(sk && sk[0] == '1')) e->sk_ctas = csk::decode_sk_ctas_per_sm(e->D, e->G, e->sk_stages) * e->sms;
+          // CS_K1_SK_WAVES=w: w x (resident CTAs) equal ranges, so the block
+          // scheduler rebalances the later waves across SMs that stream faster
+          const char* wv = std::getenv("CS_K1_SK_WAVES");
+          const int waves = wv ? std::max(1, std::atoi(wv)) : 1;
+          if (!(sk && sk[0] == '1')) {
+            e->sk_resident = csk::decode_sk_ctas_per_sm(e->D, e->G, e->sk_stages) * e->sms;
+            e->sk_ctas = e->sk_resident * waves;
+          }
           if (e->sk_ctas > 0) {
             const size_t n = static_cast<size_t>(e->sk_ctas) * 2 * e->G * (e->D + 2);
             CK(cudaMalloc(&e->ws_sk, n * 4));

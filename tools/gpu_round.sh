@@ -67,6 +67,15 @@ fi
 if has stream; then
   timeout 300 ./tools/stream_bench > "$OUT/stream_bench.jsonl" 2>&1
 fi
+if has k1wv; then
+  for shape in "39 4237" "24 4000" "50 4300"; do
+    for wv in 1 2 4; do
+      CS_K1_SK_WAVES=$wv timeout 300 python tools/decode_probe.py $shape 8 >> "$OUT/k1wv.jsonl" 2>> "$OUT/k1wv.err"
+      echo "{\"waves\": $wv, \"shape\": \"$shape\"}" >> "$OUT/k1wv.jsonl"
+    done
+  done
+  CS_K1_SK_WAVES=2 timeout 600 python -m pytest tests/test_gpu_attention.py -x -q -k k1 > "$OUT/pytest_k1wv.log" 2>&1; echo "rc=$?" >> "$OUT/pytest_k1wv.log"
+fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
