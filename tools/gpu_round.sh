@@ -76,6 +76,13 @@ if has k1wv; then
   done
   CS_K1_SK_WAVES=2 timeout 600 python -m pytest tests/test_gpu_attention.py -x -q -k k1 > "$OUT/pytest_k1wv.log" 2>&1; echo "rc=$?" >> "$OUT/pytest_k1wv.log"
 fi
+if has fusionab; then
+  timeout 900 python tools/fusion_ab.py 5 > "$OUT/fusion_ab.jsonl" 2> "$OUT/fusion_ab.err"
+  CS_NO_FUSE=0 timeout 600 $NCU --metrics gpu__time_duration.sum --csv --log-file "$OUT/fusion_launches_on.csv" \
+    python tools/fusion_ab.py child 8192 1 > /dev/null 2>&1
+  CS_NO_FUSE=1 timeout 600 $NCU --metrics gpu__time_duration.sum --csv --log-file "$OUT/fusion_launches_off.csv" \
+    python tools/fusion_ab.py child 8192 1 > /dev/null 2>&1
+fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
