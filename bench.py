@@ -624,7 +624,7 @@ def main():
                     clocks=clocks, setup_s=setup_s, kt=kt, gpu_ms=gpu_ms, step_ms=step_ms,
                     dropped=cat("dropped_layer"), drop_us=cat("drop_latency_us"), pre_drop=cat("pre_drop_layer_us"),
                     h2d=cat("h2d_bytes"), d2h=cat("d2h_bytes"), iters=int(sum(p.iterations for p in parts)),
-                    ranks_ckpt=ranks_ckpt, op_ms=op_ms)
+                    ranks_ckpt=ranks_ckpt, op_ms=op_ms, wall_end_ms=t_end)
 
     rp = replay(args.workload)
     reps = world if (world > 1 and not tp) else 1
@@ -637,7 +637,7 @@ def main():
             pre, dec = pl[pl[:, 3] != 1], pl[pl[:, 3] == 1]
             shapes.append([len(pl), int(pre[:, 1].sum()), int((pre[:, 1] * (pre[:, 1] + pre[:, 2])).sum()),
                            len(dec), int(dec[:, 2].sum())])
-        np.savez(args.dump, gpu_ms=rp["gpu_ms"], shapes=np.array(shapes, np.int64))
+        np.savez(args.dump, gpu_ms=rp["gpu_ms"], shapes=np.array(shapes, np.int64), wall_end_ms=rp["wall_end_ms"])
 
     legs = {}
     if not args.no_probes:

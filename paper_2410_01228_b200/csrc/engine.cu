@@ -431,8 +431,16 @@ struct cs_engine {
 
 namespace {
 
-int64_t DeviceMover::launch(int dir, const std::vector<csb::Segment>& segs, int64_t after_other) {
-  if (e->dry || segs.empty()) return 0;
+int64_t DeviceMover::launch(int dir, const std::vector<csb::Segment>& segs_in, int64_t after_other) {
+  if (e->dry || segs_in.empty()) return 0;
+  // Segments in host-address order (slot, then token): pages of one request
+  // usually hold adjacent host slots (in either order after LIFO reuse), so
+  // sorted they merge into a few long copy-engine runs instead of one
+  // cudaMemcpyAsync per 2 MiB page on the host's critical path.
+  std::vector<csb::Segment> segs(segs_in);
+  std::sort(segs.begin(), segs.end(), [](const csb::Segment& a, const csb::Segment& b) {
+    return a.slot != b.slot ? a.slot < b.slot : a.t0 < b.t0;
+  });
   auto ev = std::make_shared<EventPair>();
   cudaStream_t st = dir == CS_D2H ? e->s_d2h : e->s_h2d;
   // a gather reads KV the last forward wrote; either direction may have to
@@ -1672,7 +1680,7 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
         CK(cudaMalloc(&e->ws2, e->ws2_floats * 4));
         const size_t E = static_cast<size_t>(e->max_ent);
         const size_t tiles_max = static_cast<size_t>(T) * e->G / 256 + E + 1;
-        e->meta_cap = align_up(sizeof(csk::IterDesc) + 12 * static_cast<size_t>(T) + 24 * E + 4 +
+        e->meta_cap = align_up(sizeof(csk::IterDesc) + 12 * static_cast<size_t>(T) + 32 * E + 8 +
                                    (sizeof(csk::PrefillTile) + 4) * (tiles_max + 1) +
                                    4 * (static_cast<size_t>(pc.n_blocks) + E + 1) + 8 * 16,
                                1 << 20);

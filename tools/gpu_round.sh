@@ -83,6 +83,9 @@ if has fusionab; then
   CS_NO_FUSE=1 timeout 600 $NCU --metrics gpu__time_duration.sum --csv --log-file "$OUT/fusion_launches_off.csv" \
     python tools/fusion_ab.py child 8192 1 > /dev/null 2>&1
 fi
+if has dump; then
+  timeout 900 python bench.py --no-probes --legs "" --dump "$OUT/iters.npz" > "$OUT/bench_dump.json" 2> "$OUT/bench_dump.err"
+fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
