@@ -59,6 +59,9 @@ WORKLOADS = {
                 "offline backlog; TTFT SLO 150 ms, TBT SLO 100 ms; chunked prefill, 8192-token batches, 32 GiB KV "
                 "pool, safepoint every layer; 7 layer-wise drops, eviction, checkpoint and restore), scheduled with "
                 "the reference's own fit of the B200-measured latency grid (profiles/b200_fit.json)"),
+    "config1": ("config1", "tiny",
+                "config1: the reference's tiny CPU co-serving trace (2 layers, SURVEY.md 8d config 1) -- a "
+                "plumbing-size run, not a benchmark"),
     "llama8b_kv60": ("llama8b_b200_kv60", "llama8b",
                      "llama8b_b200_kv60: the same B200 schedule family on the reference's default 60 GiB KV pool "
                      "(online Gamma 3 req/s cv 2, 64-request offline backlog with replenish, no restores)"),
@@ -531,10 +534,17 @@ def main():
 
     import torch  # plumbing: device selection, barrier, max-over-ranks
     dist = None
+    one_device = os.environ.get("CS_BENCH_ONE_DEVICE") == "1"
+    red_dev = "cpu" if one_device else "cuda"  # device of the few reduced scalars
     if world > 1:
         import torch.distributed as dist
+        # CS_BENCH_ONE_DEVICE=1: every rank on GPU 0 (plumbing check of the
+        # sharded path on a one-GPU box; NCCL refuses two ranks per device, so
+        # the process group is gloo and the ranks time-slice the GPU)
+        if one_device:
+            local = 0
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group("nccl" if torch.cuda.is_available() and not one_device else "gloo")
 
     import paper_2410_01228_b200 as cs
     from paper_2410_01228_b200 import _ffi as F
@@ -555,7 +565,7 @@ def main():
         cs.engine._check(cs.lib().cs_tp_attach_ipc(eng._h, allh, world))
 
     def reduce_max(x):
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t[0])
 
@@ -608,14 +618,14 @@ def main():
         gpu_s, wall_s = float(gpu_ms.sum()) / 1e3, float(wall_ms.sum()) / 1e3
         ranks_ckpt = None
         if dist:
-            t = torch.tensor([gpu_s, wall_s], dtype=torch.float64, device="cuda")
+            t = torch.tensor([gpu_s, wall_s], dtype=torch.float64, device=red_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             gpu_s, wall_s = float(t[0]), float(t[1])
             # per-rank checkpoint traffic: every rank moves its own KV-head shard
             # over its own host link, concurrently (config 5)
             mine = torch.tensor([s1.moved_d2h_bytes - s0.moved_d2h_bytes, s1.moved_d2h_ms - s0.moved_d2h_ms,
                                  s1.moved_h2d_bytes - s0.moved_h2d_bytes, s1.moved_h2d_ms - s0.moved_h2d_ms,
-                                 s1.host_numa_node], dtype=torch.float64, device="cuda")
+                                 s1.host_numa_node], dtype=torch.float64, device=red_dev)
             allr = [torch.zeros_like(mine) for _ in range(world)]
             dist.all_gather(allr, mine)
             ranks_ckpt = [x.tolist() for x in allr]
