@@ -94,8 +94,16 @@ typedef struct cs_config {
   int32_t incremental;           /* SchedulerPolicy::incremental() */
   int32_t instrumented;          /* SchedulerPolicy::instrumented() */
   /* --- B200 data-plane sizing --- */
-  int64_t extra_blocks;          /* physical-pool slack over ceil(cap/page_bytes); <0 = auto */
-  int64_t extra_host_slots;      /* host-pool slack; <0 = auto */
+  /* Physical-pool slack over ceil(cap/page_bytes). Each live request's
+   * partial tail page counts only its tokens against the reference's byte
+   * capacity but occupies a whole block, so the pool needs one spare block
+   * per live request. <0 = auto: 2*(max_batched_tokens/16
+   * + max_entries) + 64, i.e. it assumes at most ~max_entries live requests
+   * hold partial pages; a deployment with more live (e.g. paused offline)
+   * requests sets this to its live-request bound, else allocate may fail with
+   * CS_ERR_POOL where the reference's byte accounting still succeeds. */
+  int64_t extra_blocks;
+  int64_t extra_host_slots;      /* host-pool slack (one slot per partially checkpointed page); <0 = auto: max_entries + 64 */
   int32_t max_entries;           /* max entries per plan (0 = 1024) */
   int32_t layer_lookahead;       /* unused since r2 (the forward is no longer host-paced); kept for ABI */
   /* --- sharding (KV-head groups) --- */

@@ -18,8 +18,8 @@ HQ, HKV, D = 32, 8, 128
 G = HQ // HKV
 
 
-def _engine():
-    cfg = cs.model_config("tiny", num_layers=1, hidden=512, n_heads=HQ, n_kv_heads=HKV, head_dim=D, ffn=512,
+def _engine(hq=HQ):
+    cfg = cs.model_config("tiny", num_layers=1, hidden=512, n_heads=hq, n_kv_heads=HKV, head_dim=D, ffn=512,
                           vocab=512, max_batched_tokens=4096, gpu_kv_capacity=(1 << 14) * 16 * 2 * HKV * D * 2,
                           rope_theta=500000.0, instrumented=0)
     return cs.Engine(cfg)
@@ -38,12 +38,14 @@ def _kv_of(eng, rid, n_pos):
 
 
 def _ref_rows(q, K, V, positions):
-    """q [T, HQ, D] fp32; K/V [n, HKV, D]; row t attends keys [0, positions[t]]."""
+    """q [T, hq, D] fp32; K/V [n, HKV, D]; row t attends keys [0, positions[t]]."""
     out = np.zeros_like(q)
     scale = 1.0 / np.sqrt(D)
+    hq = q.shape[1]
+    g = hq // HKV
     for t, pos in enumerate(positions):
-        for h in range(HQ):
-            s = K[:pos + 1, h // G] @ q[t, h] * scale
+        for h in range(hq):
+            s = K[:pos + 1, h // g] @ q[t, h] * scale
             s = np.exp(s - s.max())
             out[t, h] = (s / s.sum()) @ V[:pos + 1, h // G]
     return out
@@ -58,14 +60,14 @@ def _run(eng, entries, allocs):
         eng.commit_allocations(e.request_id)
 
 
-def _check_rows(eng, entries, row_pos, T):
-    qkv = N.from_bf16_bits(eng.read_activation(2, T, (HQ + 2 * HKV) * D))
-    got = N.from_bf16_bits(eng.read_activation(0, T, HQ * D)).reshape(T, HQ, D)
+def _check_rows(eng, entries, row_pos, T, hq=HQ):
+    qkv = N.from_bf16_bits(eng.read_activation(2, T, (hq + 2 * HKV) * D))
+    got = N.from_bf16_bits(eng.read_activation(0, T, hq * D)).reshape(T, hq, D)
     row = 0
     for e, positions in zip(entries, row_pos):
         n = len(positions)
         K, V = _kv_of(eng, e.request_id, max(positions) + 1)
-        q = qkv[row:row + n, :HQ * D].reshape(n, HQ, D)
+        q = qkv[row:row + n, :hq * D].reshape(n, hq, D)
         want = _ref_rows(q, K, V, positions)
         err = np.linalg.norm(got[row:row + n] - want) / np.linalg.norm(want)
         assert err <= 1e-2, (e, err)
@@ -133,6 +135,35 @@ def test_k1_stream_k_mixed_lengths(ctx):
             _run(eng, dec, [1] * len(ctx))
             _check_rows(eng, dec, [[c + rep] for c in ctx], len(ctx))
             dec = [cs.BatchEntry(r, 1, c + 2, cs.CS_DECODE, r == 0) for r, c in enumerate(ctx)]
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("hq", [40, 64])
+def test_k1_k2_other_group_sizes(hq):
+    """The Qwen-2.5-14B (40/8: G = 5) and Llama-3.1-70B (64/8: G = 8) head
+    groupings, whose K1 / K2 template instances the 8B tests never launch:
+    decode rows (stream-K K1) and a multi-tile prefill chunk in one plan."""
+    eng = _engine(hq)
+    try:
+        for r in range(4):
+            eng.register_request(r, r == 0)
+        ctx = [1, 300, 2049, 4000]
+        for r, c in enumerate(ctx):
+            _run(eng, [cs.BatchEntry(r, c, 0, cs.CS_PREFILL, r == 0)], [c + 1])
+        dec = [cs.BatchEntry(r, 1, c + 1, cs.CS_DECODE, r == 0) for r, c in enumerate(ctx)]
+        eng.register_request(9, False)
+        pre = cs.BatchEntry(9, 700, 0, cs.CS_PREFILL, False)
+        _run(eng, dec + [pre], [1] * 4 + [700])
+        _check_rows(eng, dec + [pre], [[c] for c in ctx] + [list(range(700))], 4 + 700, hq)
+        # and the per-pair split-K K1 kernel: 60 decode rows x 8 heads > resident stream-K CTAs
+        dec2 = []
+        for r in range(60):
+            eng.register_request(100 + r, False)
+            _run(eng, [cs.BatchEntry(100 + r, 200 + r, 0, cs.CS_PREFILL, False)], [201 + r])
+            dec2.append(cs.BatchEntry(100 + r, 1, 201 + r, cs.CS_DECODE, False))
+        _run(eng, dec2, [1] * 60)
+        _check_rows(eng, dec2, [[200 + r] for r in range(60)], 60, hq)
     finally:
         eng.close()
 
