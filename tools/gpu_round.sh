@@ -86,6 +86,13 @@ fi
 if has dump; then
   timeout 900 python bench.py --no-probes --legs "" --dump "$OUT/iters.npz" > "$OUT/bench_dump.json" 2> "$OUT/bench_dump.err"
 fi
+if has attn; then
+  timeout 900 python -m pytest tests/test_gpu_attention.py -q > "$OUT/pytest_attention.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_attention.log"
+fi
+if has models; then
+  timeout 1500 python bench.py --workload qwen14b --no-probes --no-cpu --legs "" > "$OUT/bench_qwen14b.json" 2> "$OUT/bench_qwen14b.err"
+  timeout 2400 python bench.py --workload llama70b --no-probes --no-cpu --legs "" > "$OUT/bench_llama70b.json" 2> "$OUT/bench_llama70b.err"
+fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
