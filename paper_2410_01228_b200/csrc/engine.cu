@@ -366,6 +366,7 @@ struct cs_engine {
   int gemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32,
            const int32_t* m_dev = nullptr, const csk::PfExtra* ex = nullptr);
   float2* rope_tab = nullptr;  // [max_tok][D/2] (cos, sin) of the iteration (K8 qkv epilogue)
+  bool kt_layer = true;        // kernel timing on for the layer being enqueued
   bool fuse_epilogues = true;  // K8 RoPE / residual epilogues (CS_NO_FUSE=1: separate kernels, for A/B)
   // Per-kernel-class device timing (cs_set_kernel_timing; bench roofline):
   // event pairs on the launching stream around every non-graph launch of
@@ -381,7 +382,7 @@ struct cs_engine {
   std::vector<std::pair<int, double>> kt_pending;  // (class, algorithmic units) per event pair
   template <typename Fn>
   void timed(int cls, double units, Fn&& fn) {
-    if (!ktime_on || it.graph) {
+    if (!ktime_on || it.graph || !kt_layer) {
       fn();
       return;
     }
@@ -959,8 +960,15 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
     csk::rope_table(rope_tab, it.ap.tok_pos, D, cfg.rope_theta, desc, T, s_compute);
     ++n_launch;
   }
+  // kernel-class timing (bench) on every kt_stride-th layer only: every
+  // layer has the same shapes, and ~16 timed layers keep a deep model's
+  // event records + launches inside the device launch queue (a full queue
+  // blocks cs_forward_launch until the GPU drains it, which would delay the
+  // caller's preemption signal by tens of layers)
+  const int kt_stride = std::max(1, (L + 15) / 16);
   for (int l = 0; l < L; ++l) {
     const int64_t M = Tg;
+    kt_layer = l % kt_stride == 0;
     if (l == 0) {
       csk::embed(x, w.emb, it.d_tok_ids, hidden, desc, T, s_compute);
     }
@@ -1054,6 +1062,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
     }
   }
   // Final norm of each entry's last row -> lm_head -> argmax.
+  kt_layer = true;
   const int E = Eg;
   csk::add_rmsnorm(x, fuse_down ? nullptr : tmp, w.final_norm, xl, hidden, cfg.rms_eps, desc, it.d_ent_last, E,
                    s_compute);

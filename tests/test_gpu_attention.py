@@ -47,7 +47,7 @@ def _ref_rows(q, K, V, positions):
         for h in range(hq):
             s = K[:pos + 1, h // g] @ q[t, h] * scale
             s = np.exp(s - s.max())
-            out[t, h] = (s / s.sum()) @ V[:pos + 1, h // G]
+            out[t, h] = (s / s.sum()) @ V[:pos + 1, h // g]
     return out
 
 
