@@ -39,6 +39,74 @@ __device__ __forceinline__ void load_page_async(uint8_t* sK, uint8_t* sV, const 
   }
 }
 
+// RoPE angle of frequency j at position pos: the same expressions as
+// rope_append_kernel / rope_table_kernel (bit-identical results).
+__device__ __forceinline__ float2 rope_cs(float pos, int j, int D, float theta) {
+  const float inv_freq = powf(theta, -2.f * static_cast<float>(j) / static_cast<float>(D));
+  float sn, cs;
+  sincosf(pos * inv_freq, &sn, &cs);
+  return make_float2(cs, sn);
+}
+
+// (x[d], x[d + D/2]) -> rotated pair, rounded to bf16 (rope_append's operations)
+__device__ __forceinline__ void rope_pair(uint32_t& lo, uint32_t& hi, float2 c0, float2 c1) {
+  const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&lo);
+  const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&hi);
+  const float2 af = __bfloat1622float2(a), bf = __bfloat1622float2(b);
+  const __nv_bfloat162 y1 = __floats2bfloat162_rn(__fmaf_rn(af.x, c0.x, -__fmul_rn(bf.x, c0.y)),
+                                                  __fmaf_rn(af.y, c1.x, -__fmul_rn(bf.y, c1.y)));
+  const __nv_bfloat162 y2 = __floats2bfloat162_rn(__fmaf_rn(bf.x, c0.x, __fmul_rn(af.x, c0.y)),
+                                                  __fmaf_rn(bf.y, c1.x, __fmul_rn(af.y, c1.y)));
+  lo = *reinterpret_cast<const uint32_t*>(&y1);
+  hi = *reinterpret_cast<const uint32_t*>(&y2);
+}
+
+// q fragments (mma.sync A layout: this thread holds dims ks*16 + tig*2 + {0,1}
+// and +8 of rows gid, gid + 8) rotated in registers; dim d pairs with d + D/2,
+// i.e. fragment ks with ks + KS/2 at the same register index.
+template <int D>
+__device__ __forceinline__ void rope_q_frags(uint32_t (*qa)[4], int tig, float pos, float theta) {
+  constexpr int KS = D / 16;
+#pragma unroll
+  for (int ks = 0; ks < KS / 2; ++ks) {
+#pragma unroll
+    for (int h8 = 0; h8 < 2; ++h8) {
+      const int d = ks * 16 + tig * 2 + h8 * 8;
+      const float2 c0 = rope_cs(pos, d, D, theta), c1 = rope_cs(pos, d + 1, D, theta);
+      rope_pair(qa[ks][2 * h8], qa[ks + KS / 2][2 * h8], c0, c1);          // row gid
+      rope_pair(qa[ks][2 * h8 + 1], qa[ks + KS / 2][2 * h8 + 1], c0, c1);  // row gid + 8
+    }
+  }
+}
+
+// The new token of a decode row: k (rotated) and v of KV head kvh from the
+// qkv row into the pool at the token's (block, slot). Called by the whole CTA
+// that will read the pair's last page, before any of that page is loaded.
+template <int D>
+__device__ __forceinline__ void append_new_kv(const AttnParams& p, int row, int kvh) {
+  const float pos = static_cast<float>(p.tok_pos[row]);
+  const int slot = p.tok_slot[row];
+  const int blk = slot >> 4, off = slot & 15;
+  __nv_bfloat16* pool = const_cast<__nv_bfloat16*>(p.pool);
+  const size_t layer_elems = static_cast<size_t>(2) * p.hkv * kPage * D;
+  __nv_bfloat16* kb = pool + (static_cast<size_t>(blk) * p.num_layers + p.layer) * layer_elems;
+  const __nv_bfloat16* src = p.qkv + static_cast<size_t>(row) * p.qkv_stride;
+  const __nv_bfloat16* k = src + static_cast<size_t>(p.hq + kvh) * D;
+  const __nv_bfloat16* v = src + static_cast<size_t>(p.hq + p.hkv + kvh) * D;
+  __nv_bfloat16* kd = kb + (static_cast<size_t>(kvh) * kPage + off) * D;
+  __nv_bfloat16* vd = kb + (static_cast<size_t>(p.hkv + kvh) * kPage + off) * D;
+  for (int j = threadIdx.x; j < D / 4; j += blockDim.x) {  // 2 frequencies per thread, bf16x2
+    uint32_t lo = *reinterpret_cast<const uint32_t*>(k + 2 * j);
+    uint32_t hi = *reinterpret_cast<const uint32_t*>(k + 2 * j + D / 2);
+    rope_pair(lo, hi, rope_cs(pos, 2 * j, D, p.rope_theta), rope_cs(pos, 2 * j + 1, D, p.rope_theta));
+    *reinterpret_cast<uint32_t*>(kd + 2 * j) = lo;
+    *reinterpret_cast<uint32_t*>(kd + 2 * j + D / 2) = hi;
+  }
+  for (int j = threadIdx.x; j < D / 8; j += blockDim.x)
+    reinterpret_cast<uint4*>(vd)[j] = reinterpret_cast<const uint4*>(v)[j];
+  __threadfence_block();
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------- K1 ----
@@ -76,6 +144,13 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
       qa[ks][1] = r1 < G ? *reinterpret_cast<const uint32_t*>(q + r1 * D + d0) : 0u;
       qa[ks][2] = r0 < G ? *reinterpret_cast<const uint32_t*>(q + r0 * D + d0 + 8) : 0u;
       qa[ks][3] = r1 < G ? *reinterpret_cast<const uint32_t*>(q + r1 * D + d0 + 8) : 0u;
+    }
+  }
+  if (p.k1_rope) {
+    rope_q_frags<D>(qa, tig, static_cast<float>(p.tok_pos[row]), p.rope_theta);
+    if (pg0 < pg1 && pg1 == n_pages) {  // this split reads the last page: the new token's K/V first
+      append_new_kv<D>(p, row, kvh);
+      __syncthreads();
     }
   }
 
@@ -338,6 +413,13 @@ __global__ void __launch_bounds__(128, 3) attn_decode_sk_kernel(AttnParams p) {
         qa[ks][1] = r1 < G ? *reinterpret_cast<const uint32_t*>(q + r1 * D + d0) : 0u;
         qa[ks][2] = r0 < G ? *reinterpret_cast<const uint32_t*>(q + r0 * D + d0 + 8) : 0u;
         qa[ks][3] = r1 < G ? *reinterpret_cast<const uint32_t*>(q + r1 * D + d0 + 8) : 0u;
+      }
+    }
+    if (p.k1_rope) {
+      rope_q_frags<D>(qa, tig, static_cast<float>(p.tok_pos[row]), p.rope_theta);
+      if (pg1 == n_i) {  // this segment reads the pair's last page: the new token's K/V first
+        append_new_kv<D>(p, row, kvh);
+        __syncthreads();
       }
     }
     float o[NTD][4];

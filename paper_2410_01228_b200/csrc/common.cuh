@@ -110,6 +110,12 @@ struct AttnParams {
   float* ws_sk;                 // K1 stream-K partials [cta][2] x {m[G], l[G], O[G][D]}
   int32_t sk_ctas;              // K1 stream-K grid (0: the split-K kernel)
   int32_t sk_stages;            // K1 stream-K per-warp ring depth (2 or 3)
+  // decode-only (CUDA-graph) iterations: K1 applies RoPE to q in registers
+  // and the CTA reading a pair's last page appends the new token's k / v
+  // (rope_append does not run); qkv then holds un-rotated q / k
+  int32_t k1_rope;
+  float rope_theta;
+  const int32_t* tok_slot;      // [T] block * 16 + slot of each token row
   int32_t k2_splits, k2_tiles_per_split;  // K2: splits over 128-key tiles
   int32_t k2_pair;                        // K2 on CTA pairs (attn_tc2.cu, head_dim 128)
   float scale_log2;             // softmax_scale * log2(e)

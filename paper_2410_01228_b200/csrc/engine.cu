@@ -956,6 +956,8 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   const bool fuse_rope = fuse_ok && D == 128 && rope_tab && use_pf(static_cast<int>(Tg), qkv_cols, hidden);
   const bool fuse_o = fuse_ok && use_pf(static_cast<int>(Tg), hidden, hq * D);
   const bool fuse_down = fuse_ok && use_pf(static_cast<int>(Tg), hidden, ffn);
+  // decode-only graphs: RoPE of q and the new token's K/V append inside K1
+  const bool k1_rope = graph && fuse_epilogues;
   if (fuse_rope) {
     csk::rope_table(rope_tab, it.ap.tok_pos, D, cfg.rope_theta, desc, T, s_compute);
     ++n_launch;
@@ -996,11 +998,15 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
       n_launch += gemm(xn, w.wqkv[l], qkv, static_cast<int>(M), qkv_cols, hidden, false, m_dev, &ex);
     } else {
       n_launch += gemm(xn, w.wqkv[l], qkv, static_cast<int>(M), qkv_cols, hidden, false, m_dev);
-      csk::rope_append(qkv, it.ap.tok_pos, it.d_tok_slot, kv, hq, hkv, D, L, l,
-                       cfg.rope_theta, desc, T, s_compute);
+      if (!k1_rope)
+        csk::rope_append(qkv, it.ap.tok_pos, it.d_tok_slot, kv, hq, hkv, D, L, l,
+                         cfg.rope_theta, desc, T, s_compute);
     }
     csk::AttnParams ap = it.ap;
     ap.layer = l;
+    ap.k1_rope = k1_rope ? 1 : 0;
+    ap.rope_theta = cfg.rope_theta;
+    ap.tok_slot = it.d_tok_slot;
     bool ok = true;
     const int n_dec_grid = graph ? Tg : it.n_dec;
     if (n_dec_grid > 0)
@@ -1054,7 +1060,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
         }
       }
     }
-    n_launch += (l == 0 ? 1 : 0) + 3 - (fuse_rope ? 1 : 0) + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
+    n_launch += (l == 0 ? 1 : 0) + 3 - (fuse_rope || k1_rope ? 1 : 0) + (tp > 1 && is_sp(l + 1) ? 1 : 0) +
                 (it.n_dec > 0 ? 1 : 0) + (it.n_pt > 0 ? (it.k2_splits > 1 ? 2 : 1) : 0);
     if ((cfg.flags & CS_FLAG_SYNC_DEBUG) && !graph) {
       CK(cudaStreamSynchronize(s_compute));

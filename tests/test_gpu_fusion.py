@@ -6,7 +6,8 @@ where the unfused kernels store (bf16 qkv / projection outputs, the same
 fma/mul rotation), so a fused engine must reproduce the unfused engine BIT
 FOR BIT: logits and every written KV block, over a Llama-3.1-8B-width
 2-layer model, a 2048-token prefill chunk (K8 path) followed by a chunk over
-that cached context and a mixed decode+prefill iteration."""
+that cached context, a mixed decode+prefill iteration, and decode-only
+CUDA-graph steps (where K1 rotates q and appends the new token's k / v)."""
 import os
 
 import numpy as np
@@ -39,8 +40,13 @@ def _run(eng):
         ([cs.BatchEntry(0, 2048, 0, cs.CS_PREFILL, False)], [(0, 2048)]),
         ([cs.BatchEntry(0, 2100, 2048, cs.CS_PREFILL, False)], [(0, 2101)]),
         ([cs.BatchEntry(1, 2200, 0, cs.CS_PREFILL, True), cs.BatchEntry(0, 1, 4149, cs.CS_DECODE, False)],
-         [(1, 2200), (0, 1)]),
+         [(1, 2201), (0, 1)]),
     ]
+    # decode-only steps (CUDA graphs): RoPE of q and the new token's K/V
+    # append run inside K1 instead of rope_append
+    for k in range(3):
+        steps.append(([cs.BatchEntry(1, 1, 2201 + k, cs.CS_DECODE, True),
+                       cs.BatchEntry(0, 1, 4150 + k, cs.CS_DECODE, False)], [(1, 1), (0, 1)]))
     for ep, (plan, allocs) in enumerate(steps):
         for rid, n in allocs:
             assert eng.allocate(rid, n).ok

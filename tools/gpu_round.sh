@@ -93,6 +93,14 @@ if has models; then
   timeout 1500 python bench.py --workload qwen14b --no-probes --no-cpu --legs "" > "$OUT/bench_qwen14b.json" 2> "$OUT/bench_qwen14b.err"
   timeout 2400 python bench.py --workload llama70b --no-probes --no-cpu --legs "" > "$OUT/bench_llama70b.json" 2> "$OUT/bench_llama70b.err"
 fi
+if has k1rope; then
+  for shape in "39 4237" "8 4237" "64 2000"; do
+    for nf in 1 0; do
+      CS_NO_FUSE=$nf timeout 300 python tools/decode_probe.py $shape 10 >> "$OUT/k1rope.jsonl" 2>> "$OUT/k1rope.err"
+      echo "{\"no_fuse\": $nf, \"shape\": \"$shape\"}" >> "$OUT/k1rope.jsonl"
+    done
+  done
+fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
