@@ -39,15 +39,6 @@ __device__ __forceinline__ void load_page_async(uint8_t* sK, uint8_t* sV, const 
   }
 }
 
-// RoPE angle of frequency j at position pos: the same expressions as
-// rope_append_kernel / rope_table_kernel (bit-identical results).
-__device__ __forceinline__ float2 rope_cs(float pos, int j, int D, float theta) {
-  const float inv_freq = powf(theta, -2.f * static_cast<float>(j) / static_cast<float>(D));
-  float sn, cs;
-  sincosf(pos * inv_freq, &sn, &cs);
-  return make_float2(cs, sn);
-}
-
 // (x[d], x[d + D/2]) -> rotated pair, rounded to bf16 (rope_append's operations)
 __device__ __forceinline__ void rope_pair(uint32_t& lo, uint32_t& hi, float2 c0, float2 c1) {
   const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&lo);
@@ -65,14 +56,14 @@ __device__ __forceinline__ void rope_pair(uint32_t& lo, uint32_t& hi, float2 c0,
 // and +8 of rows gid, gid + 8) rotated in registers; dim d pairs with d + D/2,
 // i.e. fragment ks with ks + KS/2 at the same register index.
 template <int D>
-__device__ __forceinline__ void rope_q_frags(uint32_t (*qa)[4], int tig, float pos, float theta) {
+__device__ __forceinline__ void rope_q_frags(uint32_t (*qa)[4], int tig, const float2* tab) {
   constexpr int KS = D / 16;
 #pragma unroll
   for (int ks = 0; ks < KS / 2; ++ks) {
 #pragma unroll
     for (int h8 = 0; h8 < 2; ++h8) {
       const int d = ks * 16 + tig * 2 + h8 * 8;
-      const float2 c0 = rope_cs(pos, d, D, theta), c1 = rope_cs(pos, d + 1, D, theta);
+      const float2 c0 = tab[d], c1 = tab[d + 1];
       rope_pair(qa[ks][2 * h8], qa[ks + KS / 2][2 * h8], c0, c1);          // row gid
       rope_pair(qa[ks][2 * h8 + 1], qa[ks + KS / 2][2 * h8 + 1], c0, c1);  // row gid + 8
     }
@@ -84,7 +75,7 @@ __device__ __forceinline__ void rope_q_frags(uint32_t (*qa)[4], int tig, float p
 // that will read the pair's last page, before any of that page is loaded.
 template <int D>
 __device__ __forceinline__ void append_new_kv(const AttnParams& p, int row, int kvh) {
-  const float pos = static_cast<float>(p.tok_pos[row]);
+  const float2* tab = p.rope_tab + static_cast<size_t>(row) * (D / 2);
   const int slot = p.tok_slot[row];
   const int blk = slot >> 4, off = slot & 15;
   __nv_bfloat16* pool = const_cast<__nv_bfloat16*>(p.pool);
@@ -98,7 +89,7 @@ __device__ __forceinline__ void append_new_kv(const AttnParams& p, int row, int 
   for (int j = threadIdx.x; j < D / 4; j += blockDim.x) {  // 2 frequencies per thread, bf16x2
     uint32_t lo = *reinterpret_cast<const uint32_t*>(k + 2 * j);
     uint32_t hi = *reinterpret_cast<const uint32_t*>(k + 2 * j + D / 2);
-    rope_pair(lo, hi, rope_cs(pos, 2 * j, D, p.rope_theta), rope_cs(pos, 2 * j + 1, D, p.rope_theta));
+    rope_pair(lo, hi, tab[2 * j], tab[2 * j + 1]);
     *reinterpret_cast<uint32_t*>(kd + 2 * j) = lo;
     *reinterpret_cast<uint32_t*>(kd + 2 * j + D / 2) = hi;
   }
@@ -147,7 +138,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams p) {
     }
   }
   if (p.k1_rope) {
-    rope_q_frags<D>(qa, tig, static_cast<float>(p.tok_pos[row]), p.rope_theta);
+    rope_q_frags<D>(qa, tig, p.rope_tab + static_cast<size_t>(row) * (D / 2));
     if (pg0 < pg1 && pg1 == n_pages) {  // this split reads the last page: the new token's K/V first
       append_new_kv<D>(p, row, kvh);
       __syncthreads();
@@ -416,7 +407,7 @@ __global__ void __launch_bounds__(128, 3) attn_decode_sk_kernel(AttnParams p) {
       }
     }
     if (p.k1_rope) {
-      rope_q_frags<D>(qa, tig, static_cast<float>(p.tok_pos[row]), p.rope_theta);
+      rope_q_frags<D>(qa, tig, p.rope_tab + static_cast<size_t>(row) * (D / 2));
       if (pg1 == n_i) {  // this segment reads the pair's last page: the new token's K/V first
         append_new_kv<D>(p, row, kvh);
         __syncthreads();

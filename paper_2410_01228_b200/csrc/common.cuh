@@ -115,6 +115,7 @@ struct AttnParams {
   // (rope_append does not run); qkv then holds un-rotated q / k
   int32_t k1_rope;
   float rope_theta;
+  const float2* rope_tab;       // [T][D/2] (cos, sin) of the iteration (rope_table_kernel)
   const int32_t* tok_slot;      // [T] block * 16 + slot of each token row
   int32_t k2_splits, k2_tiles_per_split;  // K2: splits over 128-key tiles
   int32_t k2_pair;                        // K2 on CTA pairs (attn_tc2.cu, head_dim 128)

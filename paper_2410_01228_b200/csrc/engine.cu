@@ -957,8 +957,8 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   const bool fuse_o = fuse_ok && use_pf(static_cast<int>(Tg), hidden, hq * D);
   const bool fuse_down = fuse_ok && use_pf(static_cast<int>(Tg), hidden, ffn);
   // decode-only graphs: RoPE of q and the new token's K/V append inside K1
-  const bool k1_rope = graph && fuse_epilogues;
-  if (fuse_rope) {
+  const bool k1_rope = graph && fuse_epilogues && rope_tab;
+  if (fuse_rope || k1_rope) {
     csk::rope_table(rope_tab, it.ap.tok_pos, D, cfg.rope_theta, desc, T, s_compute);
     ++n_launch;
   }
@@ -1007,6 +1007,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
     ap.k1_rope = k1_rope ? 1 : 0;
     ap.rope_theta = cfg.rope_theta;
     ap.tok_slot = it.d_tok_slot;
+    ap.rope_tab = rope_tab;
     bool ok = true;
     const int n_dec_grid = graph ? Tg : it.n_dec;
     if (n_dec_grid > 0)
@@ -1671,7 +1672,7 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
           // tuning timed it faster than the best cuBLAS plan, 1 always, 0 never
           const char* nf = std::getenv("CS_NO_FUSE");
           e->fuse_epilogues = !(nf && nf[0] == '1');
-          if (e->D == 128) CK(cudaMalloc(&e->rope_tab, static_cast<size_t>(e->max_tok) * (e->D / 2) * sizeof(float2)));
+          CK(cudaMalloc(&e->rope_tab, static_cast<size_t>(e->max_tok) * (e->D / 2) * sizeof(float2)));
           const char* ksk = std::getenv("CS_K7_SK");
           e->k7_sk = ksk && ksk[0] == '1';
           const char* v = std::getenv("CS_WGEMM");

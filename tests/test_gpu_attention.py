@@ -6,6 +6,8 @@ block table names. Covers multi-tile causal chunks over a cached context,
 partial pages, GQA grouping, several entries in one launch and the lazy
 O-rescale path (a late, large score). Tolerance: rel-L2 <= 1e-2 per row
 block (bf16 P/V products, fp32 accumulation)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -19,6 +21,18 @@ G = HQ // HKV
 
 
 def _engine(hq=HQ):
+    # These checks recompute attention from the q in the qkv activation, so
+    # they run the unfused path (rope_append rotates q in place); in a
+    # decode-only graph the fused path rotates q inside K1 instead -- that
+    # path is pinned bit for bit against this one by test_gpu_fusion.py.
+    os.environ["CS_NO_FUSE"] = "1"
+    try:
+        return _engine_cfg(hq)
+    finally:
+        os.environ.pop("CS_NO_FUSE", None)
+
+
+def _engine_cfg(hq):
     cfg = cs.model_config("tiny", num_layers=1, hidden=512, n_heads=hq, n_kv_heads=HKV, head_dim=D, ffn=512,
                           vocab=512, max_batched_tokens=4096, gpu_kv_capacity=(1 << 14) * 16 * 2 * HKV * D * 2,
                           rope_theta=500000.0, instrumented=0)
