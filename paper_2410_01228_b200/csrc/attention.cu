@@ -95,7 +95,9 @@ __device__ __forceinline__ void append_new_kv(const AttnParams& p, int row, int 
   }
   for (int j = threadIdx.x; j < D / 8; j += blockDim.x)
     reinterpret_cast<uint4*>(vd)[j] = reinterpret_cast<const uint4*>(v)[j];
-  __threadfence_block();
+  // the page is then read back through L2 by cp.async.cg: the stores must
+  // be performed at GPU scope first
+  __threadfence();
 }
 
 }  // namespace

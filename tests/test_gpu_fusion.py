@@ -19,17 +19,22 @@ pytestmark = pytest.mark.gpu
 
 
 def _engine(fused):
-    old = os.environ.get("CS_NO_FUSE")
-    os.environ["CS_NO_FUSE"] = "0" if fused else "1"
+    # both engines must pick the same GEMM kernels: no start-up timing (it
+    # may choose differently per engine) and cuBLASLt's heuristic choice for
+    # the decode-graph projections
+    env = {"CS_NO_FUSE": "0" if fused else "1", "CS_NO_GEMM_TUNE": "1", "CS_WGEMM": "0"}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         cfg = cs.model_config("llama8b", num_layers=2, gpu_kv_capacity=2 << 30, host_kv_capacity=1 << 28,
                               max_batched_tokens=8192, max_entries=64, instrumented=0)
         return cs.Engine(cfg)
     finally:
-        if old is None:
-            os.environ.pop("CS_NO_FUSE")
-        else:
-            os.environ["CS_NO_FUSE"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k)
+            else:
+                os.environ[k] = v
 
 
 def _run(eng):
