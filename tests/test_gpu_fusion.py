@@ -19,10 +19,11 @@ pytestmark = pytest.mark.gpu
 
 
 def _engine(fused):
-    # both engines must pick the same GEMM kernels: no start-up timing (it
-    # may choose differently per engine) and cuBLASLt's heuristic choice for
-    # the decode-graph projections
-    env = {"CS_NO_FUSE": "0" if fused else "1", "CS_NO_GEMM_TUNE": "1", "CS_WGEMM": "0"}
+    # both engines must run the same, deterministic GEMM kernels: K7 for
+    # every M <= 256 projection (a fixed-order DSMEM reduction), K8 above; no
+    # start-up timing (which may choose differently per engine) and no
+    # cuBLASLt (whose split-K reductions need not be bitwise reproducible)
+    env = {"CS_NO_FUSE": "0" if fused else "1", "CS_NO_GEMM_TUNE": "1", "CS_WGEMM": "1"}
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
