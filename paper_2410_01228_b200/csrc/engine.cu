@@ -379,7 +379,15 @@ struct cs_engine {
   bool ktime_on = false;
   KTime ktime[CS_KT_N];
   std::vector<cudaEvent_t> kt_ev;
-  std::vector<std::pair<int, double>> kt_pending;  // (class, algorithmic units) per event pair
+  // (class, algorithmic units, weight) per event pair; weight = the layer
+  // stride of the timed launch, so class totals estimate every layer
+  struct KtPending {
+    int cls;
+    double units;
+    int weight;
+  };
+  std::vector<KtPending> kt_pending;
+  int kt_weight = 1;  // weight of the launches being enqueued
   template <typename Fn>
   void timed(int cls, double units, Fn&& fn) {
     if (!ktime_on || it.graph || !kt_layer) {
@@ -395,7 +403,7 @@ struct cs_engine {
     CK(cudaEventRecord(kt_ev[2 * k], s_compute));
     fn();
     CK(cudaEventRecord(kt_ev[2 * k + 1], s_compute));
-    kt_pending.emplace_back(cls, units);
+    kt_pending.push_back({cls, units, kt_weight});
   }
   // K8 (csrc/gemm_pf.cu) for this layer GEMM? Prefill-sized M, or any
   // non-graph M > 256 when a safepoint may truncate the batch on the device
@@ -971,6 +979,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   for (int l = 0; l < L; ++l) {
     const int64_t M = Tg;
     kt_layer = l % kt_stride == 0;
+    kt_weight = std::min(kt_stride, L - l);  // this layer stands for itself and the untimed ones after it
     if (l == 0) {
       csk::embed(x, w.emb, it.d_tok_ids, hidden, desc, T, s_compute);
     }
@@ -1070,6 +1079,7 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   }
   // Final norm of each entry's last row -> lm_head -> argmax.
   kt_layer = true;
+  kt_weight = 1;
   const int E = Eg;
   csk::add_rmsnorm(x, fuse_down ? nullptr : tmp, w.final_norm, xl, hidden, cfg.rms_eps, desc, it.d_ent_last, E,
                    s_compute);
@@ -2300,10 +2310,11 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
           for (size_t k = 0; k < e->kt_pending.size(); ++k) {
             float kms = 0;
             CK(cudaEventElapsedTime(&kms, e->kt_ev[2 * k], e->kt_ev[2 * k + 1]));
-            cs_engine::KTime& t = e->ktime[e->kt_pending[k].first];
-            t.launches += 1;
-            t.ms += kms;
-            t.units += e->kt_pending[k].second;
+            const cs_engine::KtPending& kp = e->kt_pending[k];
+            cs_engine::KTime& t = e->ktime[kp.cls];
+            t.launches += kp.weight;
+            t.ms += static_cast<double>(kms) * kp.weight;
+            t.units += kp.units * kp.weight;
           }
         }
         e->kt_pending.clear();
