@@ -71,13 +71,13 @@ bool launch_attention(const AttnParams& p, const CUtensorMap* kv_map, int head_d
 int prefill_tile_rows();
 int prefill_tc2_tile_rows();
 int prefill_tile_keys();
-int wgemm_stages(int Mp, size_t budget, bool swiglu_in = false);
-int wgemm_max_clusters(int Mp, int stages, int splits, bool swiglu_in = false);
+int wgemm_stages(int Mp, size_t budget);
+int wgemm_max_clusters(int Mp, int stages, int splits);
 bool wgemm_supported(int M, int N, int K);
 void wgemm_sk(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, float* ws, int32_t* cnt, int M, int Mp,
               int N, int K, bool f32_out, int ctas, cudaStream_t s);
 void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, int Mp, int N, int K, int splits,
-              int stages, bool f32_out, cudaStream_t s, bool swiglu_in = false);
+              int stages, bool f32_out, cudaStream_t s);
 void p2p_allreduce(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s);
 void p2p_allreduce2(const P2PArgs& a, __nv_bfloat16* out, int64_t count, int blocks, cudaStream_t s);
 bool gemm_pf_supported(int N, int K);
@@ -307,9 +307,7 @@ struct cs_engine {
   std::map<std::tuple<const void*, int, int, int>, CUtensorMap> tmaps;
   const CUtensorMap* tmap(const void* p, int rows, int K, int box_rows);
   bool wgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
-  bool wgemm_launch(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32,
-                    bool swiglu_in = false);
-  bool k7_runs(int M, int N, int K, bool out_f32) const;
+  bool wgemm_launch(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K, bool out_f32);
   bool k7_sk = false;           // K7 in stream-K mode (CS_K7_SK=1; default: the cluster split-K kernel)
   float* k7_ws = nullptr;       // stream-K partials
   int32_t* k7_cnt = nullptr;    // stream-K per-tile arrival counters
@@ -836,16 +834,14 @@ bool cs_engine::wgemm(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, i
 }
 
 bool cs_engine::wgemm_launch(const __nv_bfloat16* A, const __nv_bfloat16* W, void* C, int M, int N, int K,
-                             bool out_f32, bool swiglu_in) {
+                             bool out_f32) {
   if (!csk::wgemm_supported(M, N, K)) return false;
   const int Mp = (M + 15) / 16 * 16;
-  // X rows past M are out of the tensor: TMA fills them with zeros. With
-  // swiglu_in, A is the interleaved gate|up tensor [M][2K] and K7 forms
-  // X = silu(gate) * up in shared memory
+  // X rows past M are out of the tensor: TMA fills them with zeros
   const CUtensorMap* wm = tmap(W, N, K, 128);
-  const CUtensorMap* xm = tmap(A, M, swiglu_in ? 2 * K : K, Mp);
+  const CUtensorMap* xm = tmap(A, M, K, Mp);
   if (!wm || !xm) return false;
-  if (k7_sk && !swiglu_in) {  // stream-K mode: one persistent CTA per SM, equal weight ranges
+  if (k7_sk) {  // stream-K mode: one persistent CTA per SM, equal weight ranges
     if (!k7_ws || N / 128 > 8192) return false;
     csk::wgemm_sk(wm, xm, C, k7_ws, k7_cnt, M, Mp, N, K, out_f32, sms, s_compute);
     return true;
@@ -858,31 +854,22 @@ bool cs_engine::wgemm_launch(const __nv_bfloat16* A, const __nv_bfloat16* W, voi
   // CTAs on 148 SMs ran at 2 TB/s, profiles/r1/k7_gemm.md).
   const int n_tiles = N / 128;
   const bool two = n_tiles >= sms;
-  const int stages = csk::wgemm_stages(Mp, two ? 112 * 1024 : 220 * 1024, swiglu_in);
+  const int stages = csk::wgemm_stages(Mp, two ? 112 * 1024 : 220 * 1024);
   int splits = 1;
   if (!two) {
     for (int sp = 8; sp >= 2; --sp) {
       if (n_tiles * sp > sms || K / 64 / sp < 4) continue;
-      auto key = std::make_pair(Mp * (swiglu_in ? -1 : 1), sp);
+      auto key = std::make_pair(Mp, sp);
       auto f = k7_clusters.find(key);
-      if (f == k7_clusters.end())
-        f = k7_clusters.emplace(key, csk::wgemm_max_clusters(Mp, stages, sp, swiglu_in)).first;
+      if (f == k7_clusters.end()) f = k7_clusters.emplace(key, csk::wgemm_max_clusters(Mp, stages, sp)).first;
       if (f->second >= n_tiles) {
         splits = sp;
         break;
       }
     }
   }
-  csk::wgemm_tc(wm, xm, C, M, Mp, N, K, splits, stages, out_f32, s_compute, swiglu_in);
+  csk::wgemm_tc(wm, xm, C, M, Mp, N, K, splits, stages, out_f32, s_compute);
   return true;
-}
-
-// Would gemm() run K7 for this projection (decode-sized M)?
-bool cs_engine::k7_runs(int M, int N, int K, bool out_f32) const {
-  if (wgemm_mode == 0 || !csk::wgemm_supported(M, N, K) || use_pf(M, N, K)) return false;
-  if (wgemm_mode == 1) return true;
-  auto f = k7_pick.find(lt_key(M, N, K, out_f32));
-  return f != k7_pick.end() && f->second;
 }
 
 bool cs_engine::use_pf(int M, int N, int K) const {
@@ -979,9 +966,6 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   const bool fuse_down = fuse_ok && use_pf(static_cast<int>(Tg), hidden, ffn);
   // decode-only graphs: RoPE of q and the new token's K/V append inside K1
   const bool k1_rope = graph && fuse_epilogues && rope_tab;
-  // decode projections on K7: the down projection forms its SwiGLU input
-  const bool fuse_silu = fuse_epilogues && gu_interleave && !use_pf(static_cast<int>(Tg), 2 * ffn, hidden) &&
-                         k7_runs(static_cast<int>(Tg), hidden, ffn, false);
   if (fuse_rope || k1_rope) {
     csk::rope_table(rope_tab, it.ap.tok_pos, D, cfg.rope_theta, desc, T, s_compute);
     ++n_launch;
@@ -1064,27 +1048,10 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
       n_launch += 1;
     } else {
       n_launch += gemm(xn, w.wgu[l], gu, static_cast<int>(M), 2 * ffn, hidden, false, m_dev);
-      if (!fuse_silu) {
-        csk::silu_mul(gu, act, ffn, desc, T, s_compute, gu_interleave);
-        n_launch += 1;
-      }
+      csk::silu_mul(gu, act, ffn, desc, T, s_compute, gu_interleave);
+      n_launch += 1;
     }
-    if (fuse_silu) {  // decode: K7 forms silu(gate) * up in smem from gu (no silu_mul launch)
-      __nv_bfloat16* part = partial_out(tmp);
-      if (!wgemm_launch(gu, w.wd[l], part, static_cast<int>(M), hidden, ffn, false, true))
-        throw CudaError("K7 SwiGLU-input launch failed");
-      ++n_launch;
-      if (tp > 1) {
-        if (part != tmp) ++n_launch;
-        if (is_sp(l + 1)) {
-          csk::safepoint_vote(part + M * hidden, desc, mailbox_dev, s_compute);
-          reduce_into(tmp, M * hidden + 8);
-          CK(cudaMemcpyAsync(tail, tmp + M * hidden, 16, cudaMemcpyDeviceToDevice, s_compute));
-        } else {
-          reduce_into(tmp, M * hidden);
-        }
-      }
-    } else if (fuse_down) {  // x += act . Wd^T in K8's epilogue
+    if (fuse_down) {  // x += act . Wd^T in K8's epilogue
       csk::PfExtra ex;
       ex.resid = x;
       n_launch += gemm(act, w.wd[l], tmp, static_cast<int>(M), hidden, ffn, false, m_dev, &ex);

@@ -59,7 +59,6 @@ struct WgemmArgs {
   int32_t chunks;     // 64-element K chunks per split
   int32_t f32_out;
   int32_t stages;     // smem ring depth (<= kMaxStages)
-  int32_t swiglu_in;  // X = silu(gate) * up of a gate|up (128-col interleaved) tensor, formed in smem
 };
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -68,19 +67,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int Mp = a.Mp;
-  // stage: [W 16 KB][X Mp x 128 B] (+ [gate][up] Mp x 128 B each in swiglu_in mode)
-  const uint32_t xbytes = static_cast<uint32_t>(Mp) * 128;
-  const uint32_t stage_bytes = kWBytes + xbytes * (a.swiglu_in ? 3u : 1u);  // multiple of 2 KB
-  const uint32_t tx_bytes = kWBytes + xbytes * (a.swiglu_in ? 2u : 1u);     // bytes TMA lands per stage
+  const uint32_t stage_bytes = kWBytes + static_cast<uint32_t>(Mp) * 128;  // multiple of 2 KB
   const int S = a.stages;
   const uint32_t ring_bytes = S * stage_bytes;
   const uint32_t red_bytes = static_cast<uint32_t>(Mp) * kFeat * 4;        // fp32 partial [Mp][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (ring_bytes > red_bytes ? ring_bytes : red_bytes));
-  uint64_t* full = bars;                 // [stages] TMA landed
+  uint64_t* full = bars;                 // [stages]
   uint64_t* empty = bars + kMaxStages;   // [stages]
   uint64_t* done = bars + 2 * kMaxStages;
-  uint64_t* xfull = done + 1;            // [stages] swiglu_in: X formed in smem
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(xfull + kMaxStages);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * kFeat;
@@ -92,7 +87,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int i = 0; i < S; ++i) {
       tc::mbar_init(&full[i], 1);
       tc::mbar_init(&empty[i], 1);
-      tc::mbar_init(&xfull[i], 2);  // the two SwiGLU warps
     }
     tc::mbar_init(done, 1);
     tc::fence_mbar_init();
@@ -117,7 +111,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (tc::elect_one_sync()) {
       for (int i = 0; i < pre; ++i) {
         const int kc = (c_begin + (i + rot) % nc) * kKc;
-        tc::mbar_expect_tx(&full[i], tx_bytes);
+        tc::mbar_expect_tx(&full[i], stage_bytes);
         tc::tma_load_2d(smem + i * stage_bytes, &wmap, &full[i], kc, n0);
       }
     }
@@ -132,18 +126,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // every CTA of a split needs is not fetched by all of them at once
         const int kc = (c_begin + (i + rot) % nc) * kKc;
         if (i >= pre) {
-          tc::mbar_expect_tx(&full[st], tx_bytes);
+          tc::mbar_expect_tx(&full[st], stage_bytes);
           tc::tma_load_2d(sw, &wmap, &full[st], kc, n0);
         }
-        if (a.swiglu_in) {
-          // the 64 act columns [kc, kc + 64): gate and up halves of their
-          // 128-column block of the interleaved gate|up tensor
-          const int g0 = (kc >> 7) * 256 + (kc & 127);
-          tc::tma_load_2d(sw + kWBytes + xbytes, &xmap, &full[st], g0, 0);
-          tc::tma_load_2d(sw + kWBytes + 2 * xbytes, &xmap, &full[st], g0 + 128, 0);
-        } else {
-          tc::tma_load_2d(sw + kWBytes, &xmap, &full[st], kc, 0);
-        }
+        tc::tma_load_2d(sw + kWBytes, &xmap, &full[st], kc, 0);
       }
       __syncwarp();
     }
@@ -153,7 +139,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t base = tc::smem_u32(smem);
     for (int i = 0; i < nc; ++i) {
       const int st = i % S;
-      tc::mbar_wait(a.swiglu_in ? &xfull[st] : &full[st], (i / S) & 1);
+      tc::mbar_wait(&full[st], (i / S) & 1);
       tc::tc_fence_after();
       if (tc::elect_one_sync()) {
         const uint32_t wa = base + st * stage_bytes, xa = wa + kWBytes;
@@ -165,34 +151,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (i == nc - 1) tc::umma_commit(done);
       }
       __syncwarp();
-    }
-  } else if (a.swiglu_in) {
-    // ---------------------------------------------- SwiGLU of the X tile --
-    // warps 2-3: act = silu(gate) * up for the stage's Mp x 64 tile, the
-    // same expression and bf16 rounding as silu_mul_kernel; gate, up and X
-    // share the SWIZZLE_128B layout, so the map is elementwise per 16 B
-    for (int i = 0; i < nc; ++i) {
-      const int st = i % S;
-      tc::mbar_wait(&full[st], (i / S) & 1);
-      uint8_t* sx = smem + st * stage_bytes + kWBytes;
-      const uint4* g = reinterpret_cast<const uint4*>(sx + xbytes);
-      const uint4* u = reinterpret_cast<const uint4*>(sx + 2 * xbytes);
-      uint4* x = reinterpret_cast<uint4*>(sx);
-      for (int c = threadIdx.x - 64; c < Mp * 8; c += 64) {
-        const uint4 gv = g[c], uv = u[c];
-        const __nv_bfloat16* ge = reinterpret_cast<const __nv_bfloat16*>(&gv);
-        const __nv_bfloat16* ue = reinterpret_cast<const __nv_bfloat16*>(&uv);
-        __nv_bfloat16 o[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float gf = __bfloat162float(ge[j]);
-          o[j] = __float2bfloat16(gf / (1.f + __expf(-gf)) * __bfloat162float(ue[j]));
-        }
-        x[c] = *reinterpret_cast<const uint4*>(o);
-      }
-      tc::fence_async_smem();  // generic smem writes -> the UMMA's async proxy
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&xfull[st]);
     }
   }
 
@@ -500,16 +458,17 @@ void wgemm_sk(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, float* 
   cudaLaunchKernelEx(&cfg, wgemm_sk_kernel, *wmap, *xmap, a);
 }
 
-size_t wgemm_smem_bytes(int Mp, int stages, bool swiglu_in) {
-  const size_t stage = kWBytes + static_cast<size_t>(Mp) * 128 * (swiglu_in ? 3 : 1);
+size_t wgemm_smem_bytes(int Mp, int stages) {
+  const size_t stage = kWBytes + static_cast<size_t>(Mp) * 128;
   const size_t ring = stages * stage, red = static_cast<size_t>(Mp) * kFeat * 4;
   return (ring > red ? ring : red) + 256 + 1024;
 }
 
 // Ring depth that fits `budget` bytes of shared memory (>= 2).
-int wgemm_stages(int Mp, size_t budget, bool swiglu_in) {
+int wgemm_stages(int Mp, size_t budget) {
+  const size_t stage = kWBytes + static_cast<size_t>(Mp) * 128;
   int s = kMaxStages;
-  while (s > 2 && wgemm_smem_bytes(Mp, s, swiglu_in) > budget) --s;
+  while (s > 2 && wgemm_smem_bytes(Mp, s) > budget) --s;
   return s;
 }
 
@@ -519,7 +478,7 @@ bool wgemm_supported(int M, int N, int K) { return M >= 1 && M <= 256 && N % kFe
 // xmap: X as [rows][K] (box 64 x Mp). splits x chunks covers K / 64; the K
 // splits of a feature tile are one cluster.
 void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, int Mp, int N, int K, int splits,
-              int stages, bool f32_out, cudaStream_t s, bool swiglu_in) {
+              int stages, bool f32_out, cudaStream_t s) {
   smem_attr_once(reinterpret_cast<const void*>(wgemm_tc_kernel), 227 * 1024);
   WgemmArgs a{};
   a.y = y;
@@ -532,11 +491,10 @@ void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, 
   a.splits = (total + a.chunks - 1) / a.chunks;
   a.f32_out = f32_out ? 1 : 0;
   a.stages = stages;
-  a.swiglu_in = swiglu_in ? 1 : 0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(N / kFeat, a.splits, 1);
   cfg.blockDim = dim3(kGemmThreads, 1, 1);
-  cfg.dynamicSmemBytes = wgemm_smem_bytes(Mp, stages, swiglu_in);
+  cfg.dynamicSmemBytes = wgemm_smem_bytes(Mp, stages);
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -551,12 +509,12 @@ void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, 
 }
 
 // Clusters of `splits` CTAs (each `smem` bytes) that can be resident at once.
-int wgemm_max_clusters(int Mp, int stages, int splits, bool swiglu_in) {
+int wgemm_max_clusters(int Mp, int stages, int splits) {
   smem_attr_once(reinterpret_cast<const void*>(wgemm_tc_kernel), 227 * 1024);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(1, splits, 1);
   cfg.blockDim = dim3(kGemmThreads, 1, 1);
-  cfg.dynamicSmemBytes = wgemm_smem_bytes(Mp, stages, swiglu_in);
+  cfg.dynamicSmemBytes = wgemm_smem_bytes(Mp, stages);
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 1;

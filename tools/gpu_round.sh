@@ -102,7 +102,7 @@ if has k1rope; then
   done
 fi
 if has fusiontest; then
-  timeout 900 python -m pytest tests/test_gpu_fusion.py tests/test_gpu_wgemm.py -q > "$OUT/pytest_fusion.log" 2>&1; echo "rc=$?" >> "$OUT/pytest_fusion.log"
+  timeout 900 python -m pytest tests/test_gpu_fusion.py -q > "$OUT/pytest_fusion.log" 2>&1; echo "rc=$?" >> "$OUT/pytest_fusion.log"
 fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
