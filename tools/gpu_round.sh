@@ -104,6 +104,14 @@ fi
 if has fusiontest; then
   timeout 900 python -m pytest tests/test_gpu_fusion.py -q > "$OUT/pytest_fusion.log" 2>&1; echo "rc=$?" >> "$OUT/pytest_fusion.log"
 fi
+if has wgemmab; then
+  for shape in "39 4237" "16 4237" "56 4300"; do
+    for w in 2 1 0; do
+      CS_WGEMM=$w timeout 300 python tools/decode_probe.py $shape 10 >> "$OUT/wgemmab.jsonl" 2>> "$OUT/wgemmab.err"
+      echo "{\"wgemm\": $w, \"shape\": \"$shape\"}" >> "$OUT/wgemmab.jsonl"
+    done
+  done
+fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
