@@ -14,6 +14,8 @@
 // kernel. Warp roles (128 threads): warp 0 TMA producer, warp 1 UMMA issuer
 // (one elected lane each, warp-wide loops), then all four warps drain TMEM
 // (warp w owns lanes / features 32w .. 32w+31).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -503,8 +505,16 @@ void wgemm_tc(const CUtensorMap* wmap, const CUtensorMap* xmap, void* y, int M, 
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: see the producer
   at[1].val.programmaticStreamSerializationAllowed = 1;
+  // PDL off by default: in a decode graph the early-resident K7 CTAs (one per
+  // SM, 227 KB of smem) hold SMs the producer's last CTAs need, which cost
+  // more than the weight prefetch won (39 x 4.2K step 7.144 -> 7.093 ms
+  // without it, profiles/r2/SUMMARY.md); CS_K7_PDL=1 re-enables it
+  static const bool no_pdl = [] {
+    const char* v = std::getenv("CS_K7_PDL");
+    return !(v && v[0] == '1');
+  }();
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = no_pdl ? 1 : 2;
   cudaLaunchKernelEx(&cfg, wgemm_tc_kernel, *wmap, *xmap, a);
 }
 

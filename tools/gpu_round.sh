@@ -112,6 +112,16 @@ if has wgemmab; then
     done
   done
 fi
+if has k7pdl; then
+  for shape in "39 4237" "56 4300"; do
+    for np in 0 1; do
+      CS_K7_NO_PDL=$np timeout 300 python tools/decode_probe.py $shape 10 >> "$OUT/k7pdl.jsonl" 2>> "$OUT/k7pdl.err"
+      echo "{\"no_pdl\": $np, \"shape\": \"$shape\"}" >> "$OUT/k7pdl.jsonl"
+    done
+    CS_WGEMM=0 timeout 300 python tools/decode_probe.py $shape 10 >> "$OUT/k7pdl.jsonl" 2>> "$OUT/k7pdl.err"
+    echo "{\"no_pdl\": \"cublas\", \"shape\": \"$shape\"}" >> "$OUT/k7pdl.jsonl"
+  done
+fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
