@@ -355,41 +355,19 @@ __global__ void __launch_bounds__(128, 3) attn_decode_sk_kernel(AttnParams p) {
   constexpr int kMinPages = 16;      // >= 4 pages per warp
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ int s_last;
-  __shared__ int s_unit;
   const int n_dec = p.desc->n_dec_cur;
   if (n_dec <= 0) return;
   const int hkv = p.hkv;
   const int total = hkv * p.dec_pfx[n_dec];
-  const int NG = static_cast<int>(gridDim.x);
-  // Work units: one static unit of Ws pages per CTA; with sk_dyn the static
-  // units cover 7/8 of the pages and the rest is a tail of Wd-page units the
-  // CTAs that finish first take from an atomic counter (per-SM bandwidth
-  // differs by ~10%, which equal static ranges cannot absorb). Partials and
-  // folds are keyed by unit, not by the CTA that ran it.
-  int Ws, static_end, Wd, n_units;
-  if (p.sk_dyn) {
-    Ws = max(kMinPages, static_cast<int>((static_cast<long long>(total) * 7 / 8 + NG - 1) / NG));
-    static_end = min(total, Ws * NG);
-    Wd = max(kMinPages, Ws / 4);
-    n_units = NG + (total - static_end + Wd - 1) / Wd;
-  } else {
-    Ws = max(kMinPages, (total + NG - 1) / NG);
-    static_end = total;
-    Wd = 1;
-    n_units = NG;
-  }
-  auto unit_start = [&](int u) { return u < NG ? u * Ws : static_end + (u - NG) * Wd; };
-  auto unit_end = [&](int u) { return u < NG ? min(static_end, (u + 1) * Ws) : min(total, static_end + (u - NG + 1) * Wd); };
-  auto unit_of = [&](int gp) { return gp < static_end ? gp / Ws : NG + (gp - static_end) / Wd; };
+  const int W = max(kMinPages, (total + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x));
+  const int c = blockIdx.x;
+  const int g_begin = c * W;
+  const int g_end = min(total, g_begin + W);
+  if (g_begin >= g_end) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   constexpr int kPart = G * (D + 2);  // floats per partial: m[G], l[G], O[G][D]
 
-  int c = blockIdx.x;  // the unit being run (static first, then dynamic ones)
-  for (;;) {
-  const int g_begin = min(unit_start(c), total);
-  const int g_end = unit_end(c);
-  if (g_begin < g_end) {
   // first decode entry of the range: largest i with hkv * pfx[i] <= g_begin
   int i;
   {
@@ -584,8 +562,8 @@ __global__ void __launch_bounds__(128, 3) attn_decode_sk_kernel(AttnParams p) {
       }
     }
     if (!full) {
-      // the last of the pair's covering units folds their partials
-      const int c_first = unit_of(P), c_last = unit_of(P + n_i - 1);
+      // the last of the pair's covering CTAs folds their partials
+      const int c_first = P / W, c_last = (P + n_i - 1) / W;
       __threadfence();
       __syncthreads();
       int32_t* cnt = p.dec_cnt + static_cast<size_t>(i) * hkv + kvh;
@@ -599,14 +577,14 @@ __global__ void __launch_bounds__(128, 3) attn_decode_sk_kernel(AttnParams p) {
           float M = -INFINITY;
           for (int k = 0; k < nseg; ++k) {
             const int cc = c_first + k;
-            const float* pp = p.ws_sk + (static_cast<size_t>(cc) * 2 + (unit_start(cc) >= P ? 0 : 1)) * kPart;
+            const float* pp = p.ws_sk + (static_cast<size_t>(cc) * 2 + (cc * W >= P ? 0 : 1)) * kPart;
             M = fmaxf(M, __ldcg(pp + r));
           }
           float L = 0.f, O = 0.f;
           if (M != -INFINITY) {
             for (int k = 0; k < nseg; ++k) {
               const int cc = c_first + k;
-              const float* pp = p.ws_sk + (static_cast<size_t>(cc) * 2 + (unit_start(cc) >= P ? 0 : 1)) * kPart;
+              const float* pp = p.ws_sk + (static_cast<size_t>(cc) * 2 + (cc * W >= P ? 0 : 1)) * kPart;
               const float ms = __ldcg(pp + r);
               const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
               L += __ldcg(pp + G + r) * f;
@@ -620,20 +598,6 @@ __global__ void __launch_bounds__(128, 3) attn_decode_sk_kernel(AttnParams p) {
       }
     }
     __syncthreads();  // smem (merge scratch = K/V ring) is free for the next segment
-  }
-  }  // unit non-empty
-  if (!p.sk_dyn) break;
-  if (threadIdx.x == 0) s_unit = NG + atomicAdd(p.sk_cnt, 1);
-  __syncthreads();
-  c = s_unit;
-  __syncthreads();
-  if (c >= n_units) break;
-  }  // units
-  // the last CTA out re-arms the tail counter for the next launch
-  if (p.sk_dyn && threadIdx.x == 0 && atomicAdd(p.sk_cnt + 1, 1) == NG - 1) {
-    p.sk_cnt[0] = 0;
-    p.sk_cnt[1] = 0;
-    __threadfence();
   }
 }
 

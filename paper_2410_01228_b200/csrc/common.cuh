@@ -110,8 +110,6 @@ struct AttnParams {
   float* ws_sk;                 // K1 stream-K partials [cta][2] x {m[G], l[G], O[G][D]}
   int32_t sk_ctas;              // K1 stream-K grid (0: the split-K kernel)
   int32_t sk_stages;            // K1 stream-K per-warp ring depth (2 or 3)
-  int32_t sk_dyn;               // K1 stream-K: dynamic tail units (atomic counter)
-  int32_t* sk_cnt;              // [2] tail-unit counter, finished-CTA counter (self-resetting)
   // decode-only (CUDA-graph) iterations: K1 applies RoPE to q in registers
   // and the CTA reading a pair's last page appends the new token's k / v
   // (rope_append does not run); qkv then holds un-rotated q / k

@@ -264,8 +264,6 @@ struct cs_engine {
   float* ws_sk = nullptr;      // K1 stream-K partials
   int sk_ctas = 0;             // K1 stream-K grid (0: split-K kernel)
   int sk_resident = 0;         // K1 stream-K CTAs resident at once (the kernel choice threshold)
-  bool sk_dyn = false;         // K1 stream-K dynamic tail units (CS_K1_DYN=1)
-  int32_t* sk_cnt = nullptr;   // its self-resetting counters
   int sk_stages = 2;           // K1 stream-K per-warp ring depth (CS_K1_STAGES=3 for A/B)
   // host time per forward (CS_HOST_TIMERS=1 prints the totals at cs_destroy)
   double host_prep_ms = 0, host_enq_ms = 0, host_wait_ms = 0, host_post_ms = 0;
@@ -1410,8 +1408,6 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     it.k1_sk = e->sk_ctas > 0 && it.n_dec * e->hkv < e->sk_resident;
     ap.sk_ctas = it.k1_sk ? e->sk_ctas : 0;
     ap.sk_stages = e->sk_stages;
-    ap.sk_dyn = e->sk_dyn ? 1 : 0;
-    ap.sk_cnt = e->sk_cnt;
     ap.tiles = reinterpret_cast<const csk::PrefillTile*>(d + o_tiles);
     ap.tile_order = reinterpret_cast<const int32_t*>(d + o_tiles + sizeof(csk::PrefillTile) * tiles.size());
     ap.ws = e->ws;
@@ -1670,13 +1666,8 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
             e->sk_ctas = e->sk_resident * waves;
           }
           if (e->sk_ctas > 0) {
-            // partial slots for up to 2 units per CTA (static + dynamic tail)
-            const size_t n = static_cast<size_t>(e->sk_ctas) * 2 * 2 * e->G * (e->D + 2);
+            const size_t n = static_cast<size_t>(e->sk_ctas) * 2 * e->G * (e->D + 2);
             CK(cudaMalloc(&e->ws_sk, n * 4));
-            CK(cudaMalloc(&e->sk_cnt, 2 * sizeof(int32_t)));
-            CK(cudaMemset(e->sk_cnt, 0, 2 * sizeof(int32_t)));
-            const char* dy = std::getenv("CS_K1_DYN");
-            e->sk_dyn = dy && dy[0] == '1';
           }
         }
         CK(cudaMallocHost(&e->h_out, sizeof(csk::IterDesc) + 8 * e->max_ent));
@@ -1797,7 +1788,7 @@ int cs_destroy(cs_engine* e) {
                       static_cast<void*>(e->act), static_cast<void*>(e->xl), static_cast<void*>(e->logits),
                       static_cast<void*>(e->ws), static_cast<void*>(e->ws2), static_cast<void*>(e->dec_cnt),
                       static_cast<void*>(e->ws_sk), static_cast<void*>(e->k7_ws), static_cast<void*>(e->k7_cnt),
-                      static_cast<void*>(e->rope_tab), static_cast<void*>(e->sk_cnt),
+                      static_cast<void*>(e->rope_tab),
                       static_cast<void*>(e->d_meta),
                       static_cast<void*>(e->d_out),
                       e->blas_ws})

@@ -122,15 +122,6 @@ if has k7pdl; then
     echo "{\"no_pdl\": \"cublas\", \"shape\": \"$shape\"}" >> "$OUT/k7pdl.jsonl"
   done
 fi
-if has k1dyn; then
-  CS_K1_DYN=1 timeout 600 python -m pytest tests/test_gpu_attention.py -q -k k1 > "$OUT/pytest_k1dyn.log" 2>&1; echo "rc=$?" >> "$OUT/pytest_k1dyn.log"
-  for shape in "39 4237" "24 4000" "50 4300" "8 4237" "16 16000"; do
-    for dy in 0 1; do
-      CS_K1_DYN=$dy timeout 300 python tools/decode_probe.py $shape 10 >> "$OUT/k1dyn.jsonl" 2>> "$OUT/k1dyn.err"
-      echo "{\"dyn\": $dy, \"shape\": \"$shape\"}" >> "$OUT/k1dyn.jsonl"
-    done
-  done
-fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
