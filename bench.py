@@ -741,7 +741,7 @@ def main():
                       "under_one_layer": bool(rp["drop_us"][i] < rp["pre_drop"][i])})
     ref_drops = int(sum(1 for k in range(sl[0][0], sl[-1][1]) if tr.dropped[k] >= 0))
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:  # the CPU baseline is an N = 1 measurement (rank 0)
         try:
             log = load_log(args.workload)
             k = pick_sample(log, sl[0][0], sl[-1][1])
