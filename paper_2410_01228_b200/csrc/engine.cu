@@ -2289,10 +2289,18 @@ int cs_iter_wait(cs_engine* e, cs_iter_info* info, int32_t* out_tokens, int32_t 
       // spin on the event (the iteration's end is the host loop's critical
       // path: a yielding/blocking wait adds its wake-up latency to every
       // iteration of the serving loop)
-      for (;;) {
-        const cudaError_t q = cudaEventQuery(e->ev_end);
-        if (q == cudaSuccess) break;
-        if (q != cudaErrorNotReady) CK(q);
+      static const bool block_wait = [] {
+        const char* v = std::getenv("CS_WAIT_BLOCK");
+        return v && v[0] == '1';
+      }();
+      if (block_wait) {
+        CK(cudaEventSynchronize(e->ev_end));
+      } else {
+        for (;;) {
+          const cudaError_t q = cudaEventQuery(e->ev_end);
+          if (q == cudaSuccess) break;
+          if (q != cudaErrorNotReady) CK(q);
+        }
       }
       w1 = host_ms_now();
       float ms = 0;

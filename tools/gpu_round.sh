@@ -122,6 +122,12 @@ if has k7pdl; then
     echo "{\"no_pdl\": \"cublas\", \"shape\": \"$shape\"}" >> "$OUT/k7pdl.jsonl"
   done
 fi
+if has waitab; then
+  for wb in 0 1 0 1; do
+    CS_WAIT_BLOCK=$wb timeout 900 python bench.py --no-probes --legs "" --no-cpu >> "$OUT/waitab.jsonl" 2>> "$OUT/waitab.err"
+    echo "{\"wait_block\": $wb}" >> "$OUT/waitab.jsonl"
+  done
+fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
