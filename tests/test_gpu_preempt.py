@@ -30,6 +30,11 @@ def _cfg_slow():
 
 def test_flag_drops_offline_and_keeps_online_exact():
     drv = Driver(_cfg_slow())
+    # warm-up forward on the same kernel path (K8 at M > 256 with offline
+    # work): the first launch of each kernel loads its module, which can hold
+    # cs_forward_launch until the device has finished the whole forward
+    drv.add(9, 600, online=False)
+    drv.step([(9, None)])
     drv.add(0, 30, online=True)
     drv.add(1, 6000, online=False)
     info, lg, ref = drv.step([(0, None), (1, None)], preempt_after_launch=True)
