@@ -263,7 +263,8 @@ struct cs_engine {
   int32_t* dec_cnt = nullptr;  // K1 split-K arrival counters
   float* ws_sk = nullptr;      // K1 stream-K partials
   int sk_ctas = 0;             // K1 stream-K grid (0: split-K kernel)
-  int sk_resident = 0;         // K1 stream-K CTAs resident at once (the kernel choice threshold)
+  int sk_resident = 0;         // K1 stream-K CTAs resident at once
+  int sk_pairs_max = 0;        // K1 kernel choice: stream-K below this many pairs
   int sk_stages = 2;           // K1 stream-K per-warp ring depth (CS_K1_STAGES=3 for A/B)
   // host time per forward (CS_HOST_TIMERS=1 prints the totals at cs_destroy)
   double host_prep_ms = 0, host_enq_ms = 0, host_wait_ms = 0, host_post_ms = 0;
@@ -1405,7 +1406,7 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
     // SMs streaming (39 x 4.2K: -3.3% step time); with more pairs the
     // per-pair split-K kernel has no segment overhead (128 x 2K: -5.5%)
     // (profiles/r2/k1_streamk_ab.md). Graphs are keyed by the choice.
-    it.k1_sk = e->sk_ctas > 0 && it.n_dec * e->hkv < e->sk_resident;
+    it.k1_sk = e->sk_ctas > 0 && it.n_dec * e->hkv < e->sk_pairs_max;
     ap.sk_ctas = it.k1_sk ? e->sk_ctas : 0;
     ap.sk_stages = e->sk_stages;
     ap.tiles = reinterpret_cast<const csk::PrefillTile*>(d + o_tiles);
@@ -1664,6 +1665,10 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
           if (!(sk && sk[0] == '1')) {
             e->sk_resident = csk::decode_sk_ctas_per_sm(e->D, e->G, e->sk_stages) * e->sms;
             e->sk_ctas = e->sk_resident * waves;
+            // stream-K below this many (sequence, KV head) pairs, per-pair
+            // split-K above (CS_K1_SK_PAIRS overrides, for A/B)
+            const char* sp = std::getenv("CS_K1_SK_PAIRS");
+            e->sk_pairs_max = sp ? std::atoi(sp) : e->sk_resident;
           }
           if (e->sk_ctas > 0) {
             const size_t n = static_cast<size_t>(e->sk_ctas) * 2 * e->G * (e->D + 2);

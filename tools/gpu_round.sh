@@ -128,6 +128,16 @@ if has waitab; then
     echo "{\"wait_block\": $wb}" >> "$OUT/waitab.jsonl"
   done
 fi
+if has k1thr; then
+  for shape in "56 4300" "64 4224" "80 3000" "100 2500" "128 2000"; do
+    for thr in default 100000; do
+      if [ "$thr" = default ]; then unset CS_K1_SK_PAIRS; else export CS_K1_SK_PAIRS=$thr; fi
+      timeout 300 python tools/decode_probe.py $shape 10 >> "$OUT/k1thr.jsonl" 2>> "$OUT/k1thr.err"
+      echo "{\"thr\": \"$thr\", \"shape\": \"$shape\"}" >> "$OUT/k1thr.jsonl"
+    done
+  done
+  unset CS_K1_SK_PAIRS
+fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
