@@ -1666,9 +1666,11 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
             e->sk_resident = csk::decode_sk_ctas_per_sm(e->D, e->G, e->sk_stages) * e->sms;
             e->sk_ctas = e->sk_resident * waves;
             // stream-K below this many (sequence, KV head) pairs, per-pair
-            // split-K above (CS_K1_SK_PAIRS overrides, for A/B)
+            // split-K above: the crossover sits ~15% above one resident wave
+            // (56 x 4.3K: stream-K -1.7%; 64 x 4.2K: equal; 80+ rows: split-K
+            // better, r3s); CS_K1_SK_PAIRS overrides, for A/B
             const char* sp = std::getenv("CS_K1_SK_PAIRS");
-            e->sk_pairs_max = sp ? std::atoi(sp) : e->sk_resident;
+            e->sk_pairs_max = sp ? std::atoi(sp) : e->sk_resident * 115 / 100;
           }
           if (e->sk_ctas > 0) {
             const size_t n = static_cast<size_t>(e->sk_ctas) * 2 * e->G * (e->D + 2);
