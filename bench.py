@@ -410,7 +410,7 @@ def attention_probe(cs, F, hbm_peak, bf16_peak):
     return out
 
 
-def safepoint_overhead(cs, F, reps=8, shard=None, attach=None, reduce_max=None):
+def safepoint_overhead(cs, F, reps=20, shard=None, attach=None, reduce_max=None):
     """SPEC.md acceptance #6: the same unpreempted mixed plan (online decode +
     offline 2048-token chunk) with a safepoint every layer vs none,
     alternating engines so clock drift hits both. Under the north-star split
