@@ -85,6 +85,8 @@ void gemm_pf(const CUtensorMap* xmap, const CUtensorMap* wmap, void* y, int M, c
              bool f32_out, int sms, cudaStream_t s, bool swiglu = false, const PfExtra* ex = nullptr);
 void rope_table(float2* tab, const int32_t* tok_pos, int D, float theta, const IterDesc* desc, int grid,
                 cudaStream_t s);
+void sm_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
+void out_copy(void* h_out, const IterDesc* desc, const void* keys, int E, cudaStream_t s);
 }  // namespace csk
 
 namespace {
@@ -273,9 +275,11 @@ struct cs_engine {
   size_t ws2_floats = 0;
   uint8_t* d_meta = nullptr;
   uint8_t* h_meta = nullptr;
+  uint8_t* h_meta_dev = nullptr;  // mapped alias (the SM metadata copy reads it)
   size_t meta_cap = 0;
   uint8_t* d_out = nullptr;  // IterDesc + out ids
   uint8_t* h_out = nullptr;
+  uint8_t* h_out_dev = nullptr;   // mapped alias (the output copy kernel writes it)
   csk::PreemptMailbox* mailbox = nullptr;  // mapped pinned
   csk::PreemptMailbox* mailbox_dev = nullptr;
   int64_t clock_offset_ns = 0;  // gpu globaltimer - host CLOCK_MONOTONIC
@@ -1087,10 +1091,11 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   n_launch += gemm(xl, w.lm_head, logits, E, vocab, hidden, true);
   csk::argmax_rows(logits, vocab, reinterpret_cast<unsigned long long*>(d_out + sizeof(csk::IterDesc)), desc, E,
                    s_compute);
-  CK(cudaMemcpyAsync(d_out, d_meta, sizeof(csk::IterDesc), cudaMemcpyDeviceToDevice, s_compute));
-  CK(cudaMemcpyAsync(h_out, d_out, sizeof(csk::IterDesc) + sizeof(uint64_t) * E, cudaMemcpyDeviceToHost,
-                     s_compute));
-  n_launch += 2;
+  // descriptor + sampled-token keys straight into the mapped host outputs
+  // (no copy-engine D2H queued behind checkpoint DMAs)
+  csk::out_copy(h_out_dev, reinterpret_cast<const csk::IterDesc*>(d_meta), d_out + sizeof(csk::IterDesc), E,
+                s_compute);
+  n_launch += 3;
   return n_launch;
 }
 
@@ -1311,7 +1316,8 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
       if (e->h_meta) CK(cudaFreeHost(e->h_meta));
       e->meta_cap = align_up(total * 2, 1 << 20);
       CK(cudaMalloc(&e->d_meta, e->meta_cap));
-      CK(cudaMallocHost(&e->h_meta, e->meta_cap));
+      CK(cudaHostAlloc(&e->h_meta, e->meta_cap, cudaHostAllocMapped | cudaHostAllocPortable));
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->h_meta_dev), e->h_meta, 0));
       e->drop_graphs();
     }
     uint8_t* h = e->h_meta;
@@ -1677,7 +1683,8 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
             CK(cudaMalloc(&e->ws_sk, n * 4));
           }
         }
-        CK(cudaMallocHost(&e->h_out, sizeof(csk::IterDesc) + 8 * e->max_ent));
+        CK(cudaHostAlloc(&e->h_out, sizeof(csk::IterDesc) + 8 * e->max_ent, cudaHostAllocMapped | cudaHostAllocPortable));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->h_out_dev), e->h_out, 0));
         CKB(cublasCreate(&e->blas));
         CKB(cublasSetStream(e->blas, e->s_compute));
         CK(cudaMalloc(&e->blas_ws, 64u << 20));
@@ -1718,7 +1725,8 @@ int cs_create(const cs_config* cfg, cs_engine** out) {
                                    4 * (static_cast<size_t>(pc.n_blocks) + E + 1) + 8 * 16,
                                1 << 20);
         CK(cudaMalloc(&e->d_meta, e->meta_cap));
-        CK(cudaMallocHost(&e->h_meta, e->meta_cap));
+        CK(cudaHostAlloc(&e->h_meta, e->meta_cap, cudaHostAllocMapped | cudaHostAllocPortable));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->h_meta_dev), e->h_meta, 0));
         // cuBLASLt algorithm choice for every decode-graph bucket now, at
         // start-up, instead of inside the first iteration of each bucket
         const char* nt = std::getenv("CS_NO_GEMM_TUNE");
@@ -2082,8 +2090,7 @@ int cs_forward_launch(cs_engine* e, const cs_batch_entry* entries, int32_t n, ui
     if (it.wait_h2d > 0 && e->mover && e->mover->done_prefix(CS_H2D) < it.wait_h2d) {
       if (cudaEvent_t w = e->mover->pending_event(CS_H2D, it.wait_h2d)) CK(cudaStreamWaitEvent(e->s_compute, w, 0));
     }
-    CK(cudaMemcpyAsync(e->d_meta, e->h_meta, static_cast<size_t>(it.meta_bytes), cudaMemcpyHostToDevice,
-                       e->s_compute));
+    csk::sm_copy(e->d_meta, e->h_meta_dev, static_cast<size_t>(it.meta_bytes), e->s_compute);
     e->any_forward = true;
     it.active = true;
     it.device_m = e->use_pf(it.n_tok, (e->hq + 2 * e->hkv) * e->D, e->hidden) && !it.graph;
@@ -2108,8 +2115,7 @@ int cs_bench_attention(cs_engine* e, const cs_batch_entry* entries, int32_t n, i
   return guard([&] {
     if (!prepare_iteration(e, entries, n, 0)) throw std::logic_error("attention bench needs a device engine");
     auto& it = e->it;
-    CK(cudaMemcpyAsync(e->d_meta, e->h_meta, static_cast<size_t>(it.meta_bytes), cudaMemcpyHostToDevice,
-                       e->s_compute));
+    csk::sm_copy(e->d_meta, e->h_meta_dev, static_cast<size_t>(it.meta_bytes), e->s_compute);
     csk::AttnParams ap = it.ap;
     ap.layer = 0;
     for (int w = 0; w < 2; ++w) csk::launch_attention(ap, &e->kv_map, e->D, e->G, it.n_dec, it.n_pt, e->s_compute);

@@ -293,6 +293,40 @@ __global__ void __launch_bounds__(128) rope_append_kernel(__nv_bfloat16* qkv, co
   }
 }
 
+// Small per-iteration copies done by SMs through UVA-mapped pinned memory
+// instead of the copy engines: the plan metadata H2D before a forward and
+// the iteration descriptor + sampled-token keys D2H after it. On a copy
+// engine they would queue behind the checkpoint / restore DMA chunks of the
+// same direction (up to 256 MiB, ~5 ms) and stall the forward.
+__global__ void sm_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
+void sm_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  const int64_t n16 = static_cast<int64_t>((bytes + 15) / 16);  // both buffers are 16-B padded
+  if (n16 <= 0) return;
+  const int blocks = static_cast<int>(std::min<int64_t>(64, (n16 + 255) / 256));
+  sm_copy_kernel<<<blocks, 256, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16);
+}
+
+// desc (from the metadata) + E sampled-token keys -> the pinned host outputs
+__global__ void out_copy_kernel(uint8_t* __restrict__ h_out, const IterDesc* __restrict__ desc,
+                                const unsigned long long* __restrict__ keys, int E) {
+  const int t = threadIdx.x;
+  constexpr int kDescWords = static_cast<int>(sizeof(IterDesc) / 4);
+  for (int i = t; i < kDescWords; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(h_out)[i] = reinterpret_cast<const uint32_t*>(desc)[i];
+  unsigned long long* hk = reinterpret_cast<unsigned long long*>(h_out + sizeof(IterDesc));
+  for (int i = t; i < E; i += blockDim.x) hk[i] = keys[i];
+}
+
+void out_copy(void* h_out, const IterDesc* desc, const void* keys, int E, cudaStream_t s) {
+  out_copy_kernel<<<1, 256, 0, s>>>(static_cast<uint8_t*>(h_out), desc,
+                                     static_cast<const unsigned long long*>(keys), E);
+}
+
 // (cos, sin) of every (token, frequency) of the iteration, [token][D/2]:
 // positions are the same in every layer, so the K8 qkv epilogue reads this
 // table instead of evaluating sincos per head. Same expressions as
