@@ -1373,12 +1373,8 @@ static bool prepare_iteration(cs_engine* e, const cs_batch_entry* entries, int32
       const int ctas = it.n_pt * e->hkv * (e->k2_pair ? 2 : 1);  // SMs per unit: a CTA pair or one CTA
       const int kt = csk::prefill_tile_keys();
       const int max_kt = (max_pre_kv + kt - 1) / kt;
-      static const int k2_waves = [] {
-        const char* v = std::getenv("CS_K2_SPLIT_WAVES");
-        return v ? std::max(1, std::atoi(v)) : 1;
-      }();
       if (ctas < e->sms && max_kt >= 8) {
-        const int S2 = std::min({k2_waves * e->sms / ctas, max_kt / 4, 64});
+        const int S2 = std::min({e->sms / ctas, max_kt / 4, 64});
         if (S2 > 1) {
           it.k2_tps = (max_kt + S2 - 1) / S2;
           it.k2_splits = (max_kt + it.k2_tps - 1) / it.k2_tps;

@@ -138,11 +138,6 @@ if has k1thr; then
   done
   unset CS_K1_SK_PAIRS
 fi
-if has k2split; then
-  for wv in 1 2 3; do
-    CS_K2_SPLIT_WAVES=$wv timeout 600 python tools/k2_sweep.py 20 > "$OUT/k2split_$wv.jsonl" 2>> "$OUT/k2split.err"
-  done
-fi
 if has launches; then
   CS_NO_PACING=1 CS_PROFILE_REGION=1 timeout 1200 $NCU --profile-from-start off --metrics gpu__time_duration.sum -c 8000 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 12 --warmup 3 --no-cpu --no-probes > "$OUT/launches_bench.log" 2>&1
