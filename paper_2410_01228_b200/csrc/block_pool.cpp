@@ -45,8 +45,10 @@ BlockPool::BlockPool(const PoolConfig& cfg, Mover* mover) : cfg_(cfg), mover_(mo
   for (int64_t b = cfg.n_blocks; b-- > 0;) free_blocks_.push_back(static_cast<int32_t>(b));
   free_slots_.reserve(static_cast<size_t>(cfg.n_slots));
   for (int64_t s = cfg.n_slots; s-- > 0;) free_slots_.push_back(static_cast<int32_t>(s));
-  blk_d2h_.assign(static_cast<size_t>(cfg.n_blocks), 0);
-  blk_h2d_.assign(static_cast<size_t>(cfg.n_blocks), 0);
+  // one entry past the pool: the scratch block (scratch_block()) is returned
+  // by block_for_read and never copied, so its ordinals stay 0
+  blk_d2h_.assign(static_cast<size_t>(cfg.n_blocks) + 1, 0);
+  blk_h2d_.assign(static_cast<size_t>(cfg.n_blocks) + 1, 0);
   slot_d2h_.assign(static_cast<size_t>(cfg.n_slots), 0);
   slot_h2d_.assign(static_cast<size_t>(cfg.n_slots), 0);
 }
