@@ -1,6 +1,7 @@
 """K7, the tcgen05 weight-streaming GEMM for the M <= 256 projections
-(csrc/gemm_tc.cu; opt-in with CS_WGEMM=1 until it beats cuBLAS on the decode
-step): its output against cuBLASLt on seeded bf16 operands over the decode
+(csrc/gemm_tc.cu; chosen per decode bucket and shape against the best
+cuBLASLt plan at start-up, CS_WGEMM=2 by default; CS_WGEMM=1 forces it):
+its output against cuBLASLt on seeded bf16 operands over the decode
 bucket sizes, every cluster size it launches (K split 1..8) and fp32 output,
 and a whole forward (prefill, decode CUDA graphs) with K7 against the fp32
 oracle. Tolerance: bf16 output rounding (|K7 - cuBLAS| <= 1e-2 x max |Y|)."""
@@ -24,9 +25,10 @@ def _bench(eng, M, N, K):
 
 @pytest.fixture(scope="module", params=["stream-k", "cluster"])
 def eng(request):
-    """K7 in its default stream-K mode (one persistent CTA per SM over equal
-    (tile, K-chunk) ranges, cut tiles folded from fp32 partials) and in the
-    cluster split-K mode (CS_K7_SK=0: DSMEM reduction)."""
+    """K7 in its default cluster split-K mode (CS_K7_SK=0: the K splits of a
+    feature tile reduced through DSMEM) and in the stream-K mode (CS_K7_SK=1:
+    one persistent CTA per SM over equal (tile, K-chunk) ranges, cut tiles
+    folded from fp32 partials)."""
     old = os.environ.get("CS_K7_SK")
     os.environ["CS_K7_SK"] = "1" if request.param == "stream-k" else "0"
     try:
