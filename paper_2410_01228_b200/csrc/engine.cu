@@ -49,14 +49,14 @@ void embed(__nv_bfloat16* x, const __nv_bfloat16* emb, const int32_t* tok_ids, i
            int grid, cudaStream_t s);
 void add_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16* w, __nv_bfloat16* xn, int hidden,
                  float eps, const IterDesc* desc, const int32_t* row_idx, int grid, cudaStream_t s,
-                 const SafepointArg& sp = SafepointArg{});
+                 const SafepointArg& sp = SafepointArg{}, unsigned long long* zero_keys = nullptr);
 void silu_mul(const __nv_bfloat16* gu, __nv_bfloat16* act, int ffn, const IterDesc* desc, int grid_rows,
               cudaStream_t s, bool interleave);
 void rope_append(__nv_bfloat16* qkv, const int32_t* tok_pos, const int32_t* tok_slot, __nv_bfloat16* pool, int hq,
                  int hkv, int D, int num_layers, int layer, float theta, const IterDesc* desc, int grid,
                  cudaStream_t s);
 void argmax_rows(const float* logits, int vocab, unsigned long long* keys, const IterDesc* desc, int grid,
-                 cudaStream_t s);
+                 cudaStream_t s, bool zero = true);
 void safepoint_vote(__nv_bfloat16* tail, const IterDesc* desc, const PreemptMailbox* mb, cudaStream_t s);
 void read_globaltimer(uint64_t* mapped_out, cudaStream_t s);
 void calib_clock(volatile uint64_t* mb, cudaStream_t s);
@@ -1086,11 +1086,11 @@ int cs_engine::enqueue_body(int Tg, int Eg, bool graph) {
   kt_layer = true;
   kt_weight = 1;
   const int E = Eg;
+  auto* keys = reinterpret_cast<unsigned long long*>(d_out + sizeof(csk::IterDesc));
   csk::add_rmsnorm(x, fuse_down ? nullptr : tmp, w.final_norm, xl, hidden, cfg.rms_eps, desc, it.d_ent_last, E,
-                   s_compute);
+                   s_compute, csk::SafepointArg{}, keys);
   n_launch += gemm(xl, w.lm_head, logits, E, vocab, hidden, true);
-  csk::argmax_rows(logits, vocab, reinterpret_cast<unsigned long long*>(d_out + sizeof(csk::IterDesc)), desc, E,
-                   s_compute);
+  csk::argmax_rows(logits, vocab, keys, desc, E, s_compute, /*zero=*/false);
   // descriptor + sampled-token keys straight into the mapped host outputs
   // (no copy-engine D2H queued behind checkpoint DMAs)
   csk::out_copy(h_out_dev, reinterpret_cast<const csk::IterDesc*>(d_meta), d_out + sizeof(csk::IterDesc), E,

@@ -101,7 +101,7 @@ __device__ __forceinline__ void safepoint_check(IterDesc* desc, const SafepointA
 template <int CH>
 __global__ void add_rmsnorm_kernel(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16* w,
                                    __nv_bfloat16* xn, int hidden, float eps, const IterDesc* desc,
-                                   const int32_t* row_idx, SafepointArg sp) {
+                                   const int32_t* row_idx, SafepointArg sp, unsigned long long* zero_keys) {
   pdl_trigger();  // the next projection (K7) may start streaming its weights
   const int i = blockIdx.x;
   if (sp.mb != nullptr && i == static_cast<int>(gridDim.x) - 1) {
@@ -112,6 +112,9 @@ __global__ void add_rmsnorm_kernel(__nv_bfloat16* x, const __nv_bfloat16* add, c
     if (threadIdx.x == 0) safepoint_check(const_cast<IterDesc*>(desc), sp);
     return;
   }
+  // final norm: re-arm the argmax key of this entry row (argmax_kernel
+  // atomicMax-es into it after the lm_head), instead of a memset node
+  if (zero_keys != nullptr && threadIdx.x == 0) zero_keys[i] = 0ull;
   int r;
   if (row_idx != nullptr) {
     if (i >= desc->n_ent_cur) return;
@@ -122,6 +125,14 @@ __global__ void add_rmsnorm_kernel(__nv_bfloat16* x, const __nv_bfloat16* add, c
   }
   __nv_bfloat16* xr = x + static_cast<size_t>(r) * hidden;
   const __nv_bfloat16* ar = add ? add + static_cast<size_t>(r) * hidden : nullptr;
+  // the norm weights are loaded with x (not after the reduction): one memory
+  // round trip less on this latency-bound kernel
+  uint4 wv[CH];
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int c = (k * blockDim.x + threadIdx.x) * 8;
+    if (c < hidden) wv[k] = *reinterpret_cast<const uint4*>(w + c);
+  }
   float v[CH][8];
   float ss = 0.f;
 #pragma unroll
@@ -166,8 +177,7 @@ __global__ void add_rmsnorm_kernel(__nv_bfloat16* x, const __nv_bfloat16* add, c
   for (int k = 0; k < CH; ++k) {
     const int c = (k * blockDim.x + threadIdx.x) * 8;
     if (c >= hidden) continue;
-    const uint4 wv = *reinterpret_cast<const uint4*>(w + c);
-    const __nv_bfloat16* we = reinterpret_cast<const __nv_bfloat16*>(&wv);
+    const __nv_bfloat16* we = reinterpret_cast<const __nv_bfloat16*>(&wv[k]);
     __nv_bfloat16 outv[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) outv[j] = __float2bfloat16(v[k][j] * inv * __bfloat162float(we[j]));
@@ -177,7 +187,7 @@ __global__ void add_rmsnorm_kernel(__nv_bfloat16* x, const __nv_bfloat16* add, c
 
 void add_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16* w, __nv_bfloat16* xn, int hidden,
                  float eps, const IterDesc* desc, const int32_t* row_idx, int grid, cudaStream_t s,
-                 const SafepointArg& sp) {
+                 const SafepointArg& sp, unsigned long long* zero_keys) {
   if (grid <= 0) return;
   if (sp.mb != nullptr) ++grid;  // + the K6 CTA
   const int vec = hidden / 8;
@@ -185,11 +195,11 @@ void add_rmsnorm(__nv_bfloat16* x, const __nv_bfloat16* add, const __nv_bfloat16
   const int threads = std::min(512, ((vec + 31) / 32) * 32);
   const int ch = (vec + threads - 1) / threads;
   if (ch == 1)
-    add_rmsnorm_kernel<1><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx, sp);
+    add_rmsnorm_kernel<1><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx, sp, zero_keys);
   else if (ch == 2)
-    add_rmsnorm_kernel<2><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx, sp);
+    add_rmsnorm_kernel<2><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx, sp, zero_keys);
   else
-    add_rmsnorm_kernel<4><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx, sp);
+    add_rmsnorm_kernel<4><<<grid, threads, 0, s>>>(x, add, w, xn, hidden, eps, desc, row_idx, sp, zero_keys);
 }
 
 // ----------------------------------------------------------------- SwiGLU ----
@@ -374,9 +384,36 @@ __global__ void __launch_bounds__(256) argmax_kernel(const float* logits, int vo
   const int chunk = (vocab + gridDim.x - 1) / gridDim.x;
   const int i0 = blockIdx.x * chunk, i1 = min(vocab, i0 + chunk);
   unsigned long long best = 0;
-  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-    const unsigned long long k = argmax_key(row[i], i);
-    best = k > best ? k : best;
+  if ((vocab & 3) == 0 && (chunk & 3) == 0) {
+    // 16-byte loads, two in flight per thread (the logits are L2-resident:
+    // the scan is load-latency bound, not bandwidth bound)
+    const float4* row4 = reinterpret_cast<const float4*>(row);
+    const int j0 = i0 >> 2, j1 = i1 >> 2;
+    int j = j0 + threadIdx.x;
+    for (; j + static_cast<int>(blockDim.x) < j1; j += 2 * blockDim.x) {
+      const float4 a = row4[j], b = row4[j + blockDim.x];
+      const float va[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int idx = (e < 4 ? j : j + static_cast<int>(blockDim.x)) * 4 + (e & 3);
+        const unsigned long long k = argmax_key(va[e], idx);
+        best = k > best ? k : best;
+      }
+    }
+    for (; j < j1; j += blockDim.x) {
+      const float4 a = row4[j];
+      const float va[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const unsigned long long k = argmax_key(va[e], j * 4 + e);
+        best = k > best ? k : best;
+      }
+    }
+  } else {
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+      const unsigned long long k = argmax_key(row[i], i);
+      best = k > best ? k : best;
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long k = __shfl_xor_sync(0xffffffffu, best, o);
@@ -385,10 +422,12 @@ __global__ void __launch_bounds__(256) argmax_kernel(const float* logits, int vo
   if ((threadIdx.x & 31) == 0) atomicMax(&keys[r], best);
 }
 
+// keys[0, grid) must be zero (the final add_rmsnorm re-arms them) unless
+// `zero` asks for a memset here
 void argmax_rows(const float* logits, int vocab, unsigned long long* keys, const IterDesc* desc, int grid,
-                 cudaStream_t s) {
+                 cudaStream_t s, bool zero) {
   if (grid <= 0) return;
-  cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * grid, s);
+  if (zero) cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * grid, s);
   argmax_kernel<<<dim3(16, grid), 256, 0, s>>>(logits, vocab, keys, desc);
 }
 
